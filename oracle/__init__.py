@@ -1,0 +1,155 @@
+"""CPU oracle for the reduced QMC matrix product -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) may import this.
+The product path (paper_2305_11645_b200) never imports it and shares no code with it.
+
+Thin ctypes wrapper over oracle/rqmc_oracle.c (plain C, fp64, -ffp-contract=off), which computes
+the plain definitions of PAPER.md (P:n = line n):
+  points  x_{k,j} = {k z_j / N} + shift / digital net + Phi^-1 map
+  product Y = X A, naive triple loop in increasing j
+  Q_N     N^-1 sum_k f(x_k^T A) with Neumaier summation
+Every function is pinned by tests/test_oracle_pins.py.
+Parity unpinned: f_rows for f = CALL_MEAN_EXP (C2) and MEAN_SQ (C4) beyond the naive definition.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "rqmc_oracle.c")
+_LIB = os.path.join(_HERE, "librqmc_oracle.so")
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+               "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+class _Prob(C.Structure):
+    _fields_ = [("b", C.c_int), ("m", C.c_int), ("s", C.c_int),
+                ("w", C.POINTER(C.c_int32)), ("kind", C.c_int),
+                ("z", C.POINTER(C.c_uint64)), ("C", C.POINTER(C.c_uint64)),
+                ("shift", C.POINTER(C.c_double)), ("dshift", C.POINTER(C.c_uint64)),
+                ("map", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        dp, u64p, i64p = C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+        _lib.orc_invnorm.restype = C.c_double
+        _lib.orc_invnorm.argtypes = [C.c_double]
+        _lib.orc_points.argtypes = [C.POINTER(_Prob), C.c_int64, C.c_int64, dp, u64p]
+        _lib.orc_product.argtypes = [C.c_int64, C.c_int, C.c_int, dp, dp, dp]
+        _lib.orc_f.argtypes = [C.c_int64, C.c_int, dp, C.c_int, dp, dp]
+        _lib.orc_neumaier.restype = C.c_double
+        _lib.orc_neumaier.argtypes = [dp, C.c_int64]
+        _lib.orc_f_rows.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, i64p, C.c_int64, dp, dp, C.c_int]
+        _lib.orc_f_rows_meanid.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, i64p, C.c_int64, dp, C.c_int]
+    return _lib
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(C.POINTER(t))
+
+
+class _Holder:
+    """Keeps numpy arrays alive while the C struct points at them."""
+
+    def __init__(self, prob):
+        self.w = np.ascontiguousarray(prob.w, dtype=np.int32)
+        self.z = None if prob.z is None else np.ascontiguousarray(prob.z, dtype=np.uint64)
+        self.Cm = None if prob.C is None else np.ascontiguousarray(prob.C, dtype=np.uint64)
+        self.sh = None if prob.shift is None else np.ascontiguousarray(prob.shift, dtype=np.float64)
+        self.ds = None if prob.dshift is None else np.ascontiguousarray(prob.dshift, dtype=np.uint64)
+        self.s = _Prob(prob.b, prob.m, prob.s, _ptr(self.w, C.c_int32), prob.kind,
+                       _ptr(self.z, C.c_uint64), _ptr(self.Cm, C.c_uint64),
+                       _ptr(self.sh, C.c_double), _ptr(self.ds, C.c_uint64), prob.map)
+
+
+def invnorm(u: float) -> float:
+    return lib().orc_invnorm(float(u))
+
+
+def points(prob, k0: int = 0, n: int | None = None):
+    """(X, T): rows k0..k0+n of the point matrix X and the integer word of each entry."""
+    n = prob.N - k0 if n is None else n
+    h = _Holder(prob)
+    X = np.empty((n, prob.s), dtype=np.float64)
+    T = np.empty((n, prob.s), dtype=np.uint64)
+    lib().orc_points(C.byref(h.s), k0, n, _ptr(X, C.c_double), _ptr(T, C.c_uint64))
+    return X, T
+
+
+def product(X: np.ndarray, A: np.ndarray) -> np.ndarray:
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n, s = X.shape
+    tau = A.shape[1]
+    Y = np.empty((n, tau), dtype=np.float64)
+    lib().orc_product(n, s, tau, _ptr(X, C.c_double), _ptr(A, C.c_double), _ptr(Y, C.c_double))
+    return Y
+
+
+def f_of_y(Y: np.ndarray, f: int, fparam) -> np.ndarray:
+    Y = np.ascontiguousarray(Y, dtype=np.float64)
+    fp = np.ascontiguousarray(np.asarray(fparam, dtype=np.float64).reshape(-1)[:2].copy() if fparam is not None else np.zeros(2))
+    fk = np.empty(Y.shape[0])
+    lib().orc_f(Y.shape[0], Y.shape[1], _ptr(Y, C.c_double), f, _ptr(fp, C.c_double), _ptr(fk, C.c_double))
+    return fk
+
+
+def neumaier(v: np.ndarray) -> float:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    return lib().orc_neumaier(_ptr(v, C.c_double), len(v))
+
+
+def f_rows(prob, ks, with_y: bool = False, nthreads: int = 0, f: int | None = None):
+    """f_k (and optionally Y rows) for the given global row indices k, via O1+O2+O3."""
+    h = _Holder(prob)
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int64))
+    A = np.ascontiguousarray(prob.A, dtype=np.float64)
+    fp = np.ascontiguousarray(np.asarray(prob.fparam, dtype=np.float64))
+    fk = np.empty(len(ks))
+    Y = np.empty((len(ks), prob.tau)) if with_y else None
+    ff = prob.f if f is None else f
+    err = lib().orc_f_rows(C.byref(h.s), _ptr(A, C.c_double), prob.tau, ff, _ptr(fp, C.c_double),
+                           _ptr(ks, C.c_int64), len(ks), _ptr(fk, C.c_double), _ptr(Y, C.c_double), nthreads)
+    if err:
+        raise MemoryError("oracle f_rows allocation failed")
+    return (fk, Y) if with_y else fk
+
+
+def f_rows_meanid(prob, ks, nthreads: int = 0):
+    """O3' mean identity (g = id only): f_k = F(x_k . abar), abar = tau^-1 A 1."""
+    h = _Holder(prob)
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int64))
+    A = np.ascontiguousarray(prob.A, dtype=np.float64)
+    fk = np.empty(len(ks))
+    if lib().orc_f_rows_meanid(C.byref(h.s), _ptr(A, C.c_double), prob.tau, prob.f,
+                               _ptr(ks, C.c_int64), len(ks), _ptr(fk, C.c_double), nthreads):
+        raise ValueError("mean identity needs g = id (f in {EXP_MEAN, MEAN})")
+    return fk
+
+
+def xa(prob, k0: int = 0, n: int | None = None) -> np.ndarray:
+    """Y rows k0..k0+n of XA by the naive definition."""
+    X, _ = points(prob, k0, n)
+    return product(X, prob.A)
+
+
+def qn_sum(prob, ks=None, nthreads: int = 0) -> float:
+    """sum_k f(x_k^T A) over rows ks (default all N), Neumaier in increasing k (times N)."""
+    ks = np.arange(prob.N, dtype=np.int64) if ks is None else ks
+    return neumaier(f_rows(prob, ks, nthreads=nthreads))

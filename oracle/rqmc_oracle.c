@@ -1,0 +1,227 @@
+/*
+ * rqmc_oracle.c -- TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct CPU oracle
+ * for the reduced QMC matrix product of Dick, Ebert, Herrmann, Kritzer, Longo,
+ * "The fast reduced QMC matrix-vector product" (arXiv 2305.11645; /root/reference/PAPER.md = P:n).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+ * load this library.  It shares no code, header, table or constant with the CUDA path
+ * (paper_2305_11645_b200/csrc); the only common input is the seeded data from workloads/.
+ *
+ * What it computes: the PLAIN definition, never the reduced algorithm.
+ *   O1 points  x_k materialised from the point-set definitions:
+ *        lattice  x_{k,j} = { k z_j / N },  z_j = b^{w_j} z'_j          (first form P:307)
+ *        shift    psi(x) = { x + Delta_j }
+ *        net      vec y_{j,n} = Chat^(j) vec n, y = vec y . (b^-1..b^-m)    (Eq. def:digital)
+ *                 Chat^(j): last min(w_j,m) rows of C^(j) set to zero      (Eq. reduced_genmat_net2)
+ *        digital shift (reading C-9): V = (W << (53-m)) XOR sigma_j, x = V 2^-53
+ *        map      x = Phi^-1(u), zero rule reading C-5
+ *   O2 product Y[k,c] = sum_{j=1..s} x_{k,j} A[j,c], increasing j
+ *   O3 f_k = F(tau^-1 sum_c g(Y[k,c])) (increasing c); sum_k f_k Neumaier-compensated
+ *   O3' (g = id only) f_k = F(sum_j x_{k,j} abar_j), abar = tau^-1 A 1   -- algebraic identity, O(Ns)
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC (no FMA contraction).
+ * Parity is pinned by tests/test_oracle_pins.py (paper example, SPEC examples, closed forms,
+ * exact rational brute force, library Phi^-1); see DESIGN.md "Oracle pins".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+  int b, m, s;
+  const int32_t* w;        /* s reduction indices, 0 = w_1 <= w_2 <= ... */
+  int kind;                /* 0 lattice, 1 digital net (b = 2) */
+  const uint64_t* z;       /* lattice z'_j */
+  const uint64_t* C;       /* net: column words, C[j*m+q] bit (m-1-p) = C^(j)_{p+1,q+1} */
+  const double* shift;     /* lattice Delta_j in [0,1) or NULL */
+  const uint64_t* dshift;  /* net sigma_j < 2^53 or NULL */
+  int map;                 /* 0 identity, 1 Phi^-1 */
+} orc_problem;
+
+static uint64_t ipow(uint64_t b, int e) {
+  uint64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+/* Standard normal CDF Phi(x) = erfc(-x/sqrt 2)/2 (libm erfc). */
+static double orc_Phi(double x) { return 0.5 * erfc(-x / sqrt(2.0)); }
+
+/* Phi^-1(u): the x with Phi(x) = u.  Start from Abramowitz-Stegun 26.2.23 and refine with
+ * Halley steps on Phi(x) - q until the step stalls.  Works on q = min(u, 1-u) (x <= 0 side,
+ * where erfc is accurate in relative terms) and restores the sign (Phi^-1(1-u) = -Phi^-1(u)). */
+double orc_invnorm(double u) {
+  if (!(u > 0.0 && u < 1.0)) return NAN;
+  if (u == 0.5) return 0.0;
+  double q = u < 0.5 ? u : 1.0 - u;
+  double t = sqrt(-2.0 * log(q));
+  double x = -(t - (2.515517 + 0.802853 * t + 0.010328 * t * t) /
+                       (1.0 + 1.432788 * t + 0.189269 * t * t + 0.001308 * t * t * t));
+  for (int it = 0; it < 100; ++it) {
+    double e = orc_Phi(x) - q;
+    double phi = exp(-0.5 * x * x) / sqrt(2.0 * M_PI);
+    double dx = e / (phi + 0.5 * x * e);
+    x -= dx;
+    if (fabs(dx) <= 1e-17 * fmax(1.0, fabs(x))) break;
+  }
+  return u < 0.5 ? x : -x;
+}
+
+/* u in [0,1) -> point coordinate, with the zero rule (reading C-5). */
+static double orc_map(const orc_problem* p, double u, int shifted) {
+  if (p->map == 0) return u;
+  if (u == 0.0) u = shifted ? ldexp(1.0, -53) : 0.5 / (double)ipow((uint64_t)p->b, p->m);
+  return orc_invnorm(u);
+}
+
+/* O1: rows k in [k0, k0+n) of X (row-major n x s); T gets the integer word of each entry:
+ * lattice: (k z_j mod N) (numerator over N); net: W (unshifted m-digit word) or V (shifted 53-digit). */
+int orc_points(const orc_problem* p, int64_t k0, int64_t n, double* X, uint64_t* T) {
+  const uint64_t N = ipow((uint64_t)p->b, p->m);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t k = (uint64_t)(k0 + i);
+    for (int j = 0; j < p->s; ++j) {
+      int wj = p->w[j];
+      double u;
+      uint64_t word;
+      int shifted;
+      if (p->kind == 0) {
+        /* z_j = b^{w_j} z'_j; for w_j >= m, z_j is a multiple of N. */
+        uint64_t zj = wj >= p->m ? 0 : (uint64_t)(((unsigned __int128)ipow((uint64_t)p->b, wj) * p->z[j]) % N);
+        word = (uint64_t)(((unsigned __int128)k * zj) % N);     /* k z_j mod N */
+        u = (double)word / (double)N;                            /* { k z_j / N } */
+        shifted = p->shift != NULL;
+        if (shifted) {                                           /* psi(x) = {x + Delta}, reading C-6 */
+          u = u + p->shift[j];
+          if (u >= 1.0) u = u - 1.0;
+        }
+      } else {
+        /* digits of k, least significant first; Chat rows p > m - min(w_j,m) zeroed */
+        int keep_rows = p->m - (wj < p->m ? wj : p->m);
+        uint64_t W = 0;
+        for (int pp = 1; pp <= p->m; ++pp) {            /* output digit p (weight b^-p) */
+          if (pp > keep_rows) continue;                 /* row of Chat is zero */
+          unsigned y = 0;
+          for (int qq = 1; qq <= p->m; ++qq) {          /* input digit q */
+            unsigned kappa = (unsigned)((k >> (qq - 1)) & 1u);
+            unsigned c = (unsigned)((p->C[(size_t)j * p->m + (qq - 1)] >> (p->m - pp)) & 1u);
+            y = (y + c * kappa) % 2u;
+          }
+          W += (uint64_t)y << (p->m - pp);              /* sum_p y_p 2^{m-p} */
+        }
+        shifted = p->dshift != NULL;
+        if (shifted) {
+          word = (W << (53 - p->m)) ^ p->dshift[j];
+          u = (double)word * ldexp(1.0, -53);
+        } else {
+          word = W;
+          u = (double)W * ldexp(1.0, -p->m);
+        }
+      }
+      if (T) T[i * p->s + j] = word;
+      if (X) X[i * p->s + j] = orc_map(p, u, shifted);
+    }
+  }
+  return 0;
+}
+
+/* O2: naive product Y (n x tau) = X (n x s) A (s x tau), each Y[k,c] accumulated in increasing j. */
+void orc_product(int64_t n, int s, int tau, const double* X, const double* A, double* Y) {
+  for (int64_t k = 0; k < n; ++k) {
+    double* y = Y + k * tau;
+    for (int c = 0; c < tau; ++c) y[c] = 0.0;
+    for (int j = 0; j < s; ++j) {
+      double x = X[k * s + j];
+      const double* a = A + (size_t)j * tau;
+      for (int c = 0; c < tau; ++c) y[c] = y[c] + x * a[c];
+    }
+  }
+}
+
+/* O3: f_k = F(tau^-1 sum_c g(y_c)), c increasing (readings C-17). f ids as workloads.F_*. */
+static double orc_f_row(const double* y, int tau, int f, const double* fp) {
+  double acc = 0.0;
+  switch (f) {
+    case 0: for (int c = 0; c < tau; ++c) acc = acc + y[c]; return exp(acc / tau);
+    case 1: for (int c = 0; c < tau; ++c) acc = acc + exp(fp[0] * y[c]);
+            acc = acc / tau - fp[1]; return acc > 0.0 ? acc : 0.0;
+    case 2: for (int c = 0; c < tau; ++c) acc = acc + y[c] * y[c]; return acc / tau;
+    case 3: for (int c = 0; c < tau; ++c) acc = acc + y[c]; return acc / tau;
+    default: return NAN;
+  }
+}
+
+void orc_f(int64_t n, int tau, const double* Y, int f, const double* fp, double* fk) {
+  for (int64_t k = 0; k < n; ++k) fk[k] = orc_f_row(Y + k * tau, tau, f, fp);
+}
+
+/* Neumaier-compensated sum in increasing index. */
+double orc_neumaier(const double* v, int64_t n) {
+  double s = 0.0, c = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double t = s + v[i];
+    if (fabs(s) >= fabs(v[i])) c += (s - t) + v[i];
+    else c += (v[i] - t) + s;
+    s = t;
+  }
+  return s + c;
+}
+
+/* f_k for arbitrary rows ks[0..n) via O1+O2+O3, OpenMP over rows (order within a row fixed). */
+int orc_f_rows(const orc_problem* p, const double* A, int tau, int f, const double* fp,
+               const int64_t* ks, int64_t n, double* fk, double* Yrows /* nullable n x tau */,
+               int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  int err = 0;
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * p->s);
+    double* y = (double*)malloc(sizeof(double) * tau);
+    if (!x || !y) err = 1;
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t i = 0; i < n; ++i) {
+      if (!x || !y) continue;
+      orc_points(p, ks[i], 1, x, NULL);
+      orc_product(1, p->s, tau, x, A, y);
+      fk[i] = orc_f_row(y, tau, f, fp);
+      if (Yrows) memcpy(Yrows + i * tau, y, sizeof(double) * tau);
+    }
+    free(x);
+    free(y);
+  }
+  return err;
+}
+
+/* O3': for g = id (f in {0: exp(mean), 3: mean}): f_k = F(sum_j x_{k,j} abar_j), abar = tau^-1 A 1. */
+int orc_f_rows_meanid(const orc_problem* p, const double* A, int tau, int f, const int64_t* ks,
+                      int64_t n, double* fk, int nthreads) {
+  if (f != 0 && f != 3) return 1;
+  double* abar = (double*)malloc(sizeof(double) * p->s);
+  for (int j = 0; j < p->s; ++j) {
+    double acc = 0.0;
+    for (int c = 0; c < tau; ++c) acc = acc + A[(size_t)j * tau + c];
+    abar[j] = acc / tau;
+  }
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * p->s);
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i) {
+      orc_points(p, ks[i], 1, x, NULL);
+      double acc = 0.0;
+      for (int j = 0; j < p->s; ++j) acc = acc + x[j] * abar[j];
+      fk[i] = f == 0 ? exp(acc) : acc;
+    }
+    free(x);
+  }
+  free(abar);
+  return 0;
+}
