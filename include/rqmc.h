@@ -1,0 +1,157 @@
+/*
+ * rqmc.h -- C ABI of the B200-native reduced QMC matrix product.
+ *
+ * Computes, for the N = b^m points x_k of a reduced rank-1 lattice or a column-reduced base-2
+ * digital net (optionally randomly / digitally shifted and mapped to N(0,1)) and any dense s x tau
+ * matrix A:
+ *     Y = X A                      (X never materialised, only X^red per level)
+ *     Q_N = N^-1 sum_k f(x_k^T A)
+ * by the paper's Algorithm 2 with dense per-level products: the coordinates are grouped
+ * into levels w = min(w_j, m) (tau_I), each level is one dense product
+ * P_w = X^red_w (b^{m-w} x s_w) A_w (s_w x tau), and the rows are rebuilt by the periodic
+ * tile-accumulate R_w[r] = P_w[r] + R_w'[r mod b^{m-w'}], Y = R_0.
+ * P:n = /root/reference/PAPER.md line n;  S:n = SPEC.md line n.
+ *
+ * Conventions
+ *  - All host arrays passed to rqmc_plan_create are COPIED; the caller keeps ownership.
+ *  - Device buffers (A, Y, d_fsum, workspace) are owned by the caller (e.g. torch tensors).
+ *  - fparam is a HOST pointer to 2 doubles (may be NULL when f does not use it).
+ *  - stream is a cudaStream_t passed as void* (NULL = legacy default stream).  Run calls are
+ *    asynchronous on it; device faults surface at the caller's next synchronisation.
+ *  - Validation errors are returned synchronously; rqmc_plan_last_error() names the offending
+ *    coordinate / level.  A plan is immutable after creation (device tables are uploaded on the
+ *    first run call, thread-safely): concurrent runs on distinct streams with distinct outputs and
+ *    workspaces are safe.
+ *  - Layouts: A row-major s x tau, row j = a_j, leading dimension lda >= tau (elements).
+ *    Y row-major (N/world) x tau, ldy >= tau; local row i is global point k = rank + world * i
+ *    (residue-class partition, multi-GPU; world = 1 gives Y = XA).
+ *  - Precision: fp64 throughout.  Point indices/digits are exact integers; lattice values are
+ *    u = t/M (IEEE divide), shift u = u + Delta, if u >= 1 then u - 1 (no FMA contraction).
+ *  - Limits: N = b^m <= 2^32; m <= 53 for nets; world must be a power of b dividing N.
+ */
+#ifndef RQMC_H
+#define RQMC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rqmc_plan_s* rqmc_plan_t;
+
+typedef enum {
+  RQMC_OK = 0,
+  RQMC_EINVAL = 1,       /* null pointer / bad size / bad enum / workspace too small       */
+  RQMC_ENOTPRIME = 2,    /* b is not prime                                     */
+  RQMC_EWORDER = 3,      /* w not nondecreasing or w_1 != 0                        */
+  RQMC_EZUNIT = 4,       /* z'_j not in U_{b^{m-w_j}}                          */
+  RQMC_ESHIFT = 5,       /* shift outside [0,1) or digital shift >= 2^53                   */
+  RQMC_ENETMAT = 6,      /* net matrices: bad words, or reduced net not periodic    */
+  RQMC_EDIM = 7,         /* dimension mismatch / lda < tau / ldy < tau                     */
+  RQMC_EDOMAIN = 8,      /* Phi^-1 domain (never raised for valid plans: zero rule)        */
+  RQMC_ECUDA = 9,        /* CUDA launch / copy failure, or no device                       */
+  RQMC_ENOMEM = 10,      /* allocation failure                                             */
+  RQMC_EUNSUPPORTED = 11 /* outside the supported envelope (N > 2^32, world, ...)          */
+} rqmc_status;
+
+typedef enum { RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1 } rqmc_kind;
+typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1 } rqmc_map;
+
+/* f(y) = F(tau^-1 sum_c g(y_c))  (SURVEY reading C-17)                                    */
+typedef enum {
+  RQMC_F_NONE = -1,
+  RQMC_F_EXP_MEAN = 0,      /* exp(mean(y))                                  (C1, C3, C5)  */
+  RQMC_F_CALL_MEAN_EXP = 1, /* max(mean(exp(p0 * y)) - p1, 0)                (C2)          */
+  RQMC_F_MEAN_SQ = 2,       /* mean(y^2)                                     (C4)          */
+  RQMC_F_MEAN = 3           /* mean(y), linear                               (tests)       */
+} rqmc_f;
+
+typedef struct {
+  int b, m, s, tau;         /* b prime, N = b^m, A is s x tau                                 */
+  const int32_t* w;         /* s reduction indices, nondecreasing, w[0] == 0         */
+  rqmc_kind kind;
+  const uint64_t* z;        /* lattice: z'_j in U_{b^{m-w_j}}, s entries         */
+  const uint64_t* C;        /* net (b=2): s*m column words; bit (m-1-p) of C[j*m+q] is
+                               C^(j)_{p+1,q+1} (row p+1 = output digit, col q+1 = input digit,
+                               LSB-first).  The plan applies the paper's row zeroing
+                               (Eq. reduced_genmat_net2) and requires the result to
+                               have columns q >= m - min(w_j,m) zero (column deletion),
+                               which makes coordinate j periodic in k with period 2^{m-w_j}.  */
+  const double* shift;      /* lattice random shift Delta_j in [0,1), or NULL        */
+  const uint64_t* dshift;   /* net digital shift sigma_j < 2^53: x = ((W << (53-m)) ^ sigma) 2^-53 */
+  rqmc_map map;             /* RQMC_MAP_INVNORM: x = Phi^-1(u), u = 0 remapped (reading C-5) */
+  int rank, world;          /* residue-class partition k = rank (mod world); (0,1) = whole   */
+} rqmc_plan_desc;
+
+/* Level table entry (coarse -> fine), for inspection and tests. */
+typedef struct {
+  int w;            /* level index min(w_j, m) (m = constant level of shifted w_j >= m)        */
+  int j_lo, s_w;    /* 0-based coordinates j_lo .. j_lo+s_w-1 (tau_w = s_w)             */
+  int64_t M;        /* global distinct rows b^{m-w}                                            */
+  int64_t M_local;  /* rows on this rank: max(M / world, 1)                                    */
+  int parent;       /* index of the next coarser non-empty level, -1 for the top               */
+  int coarse;       /* 1: materialised per-level GEMM pass; 0: fused into the fine kernel      */
+} rqmc_level_info;
+
+typedef struct {
+  int n_levels;             /* non-empty levels                                              */
+  int checkpoint;           /* index of the last coarse level (root of the fine kernel)      */
+  int n_fine;               /* fused fine levels below the checkpoint                        */
+  int64_t n_bundles;        /* fine-kernel CTAs (bundles of residues of the checkpoint)      */
+  int64_t N_local;          /* N / world                                                     */
+  int s_star;               /* s* = max{j : w_j < m}                                 */
+} rqmc_plan_summary;
+
+rqmc_status rqmc_plan_create(const rqmc_plan_desc* desc, rqmc_plan_t* out);
+void        rqmc_plan_destroy(rqmc_plan_t p);
+const char* rqmc_strerror(rqmc_status s);
+const char* rqmc_plan_last_error(rqmc_plan_t p);
+
+rqmc_status rqmc_plan_summary_get(rqmc_plan_t p, rqmc_plan_summary* out);
+rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* out);
+/* Global point index k of local row i (k = rank + world*i). */
+int64_t     rqmc_plan_global_row(rqmc_plan_t p, int64_t i);
+/* Counter law: local rows, algorithmic MACs tau * sum_w M_w s_w and the
+ * minimum HBM bytes 8 s tau (+ 8 N tau when Y is stored). */
+rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* local_rows, double* macs, double* min_bytes);
+
+/* Bytes of device workspace a run needs (X^red of every level, checkpoint R buffers, partials,
+ * plus a staging copy of A for the *_host entry points). */
+rqmc_status rqmc_workspace_size(rqmc_plan_t p, size_t* bytes);
+
+/* Y = X A on this rank's rows (dY non-NULL, ldy >= tau); if f != RQMC_F_NONE and d_fsum != NULL,
+ * also writes d_fsum[0] = sum over this rank's rows of f(x_k^T A) (fixed-order reduction).
+ * Q_N = (all-reduce over ranks of d_fsum) / N. */
+rqmc_status rqmc_xa(rqmc_plan_t p, const double* dA, int64_t lda, double* dY, int64_t ldy,
+                    rqmc_f f, const double* fparam, double* d_fsum,
+                    void* dwork, size_t wbytes, void* stream);
+
+/* As rqmc_xa without storing Y (the N x tau result is consumed in registers by f). */
+rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, const double* fparam,
+                    double* d_fsum, void* dwork, size_t wbytes, void* stream);
+
+/* End-to-end form with HOST buffers: copies hA (pinned or pageable) into the workspace, runs
+ * rqmc_qn and copies the local f-sum back into *h_fsum; synchronises the stream before returning. */
+rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
+                         double* h_fsum, void* dwork, size_t wbytes, void* stream);
+
+/* Debug / parity: the reduced points of level `idx` for local rows [r0, r0+count):
+ * d_words[i*s_w+q] = integer word (lattice t = r z'_j mod M; net W or shifted V) and
+ * d_vals[i*s_w+q] = the mapped fp64 coordinate.  Either output may be NULL. */
+rqmc_status rqmc_points(rqmc_plan_t p, int idx, int64_t r0, int64_t count,
+                        uint64_t* d_words, double* d_vals, void* stream);
+
+/* Device-side phase timing for roofline reporting: while enabled (max_runs > 0) every run records
+ * CUDA events on its stream around its phases (points, coarse GEMMs, fused fine kernel, reduction);
+ * rqmc_profile_read synchronises those events and returns the summed milliseconds of the recorded
+ * runs (and how many).  max_runs = 0 disables and frees the events.  Not thread-safe per plan. */
+rqmc_status rqmc_profile_enable(rqmc_plan_t p, int max_runs);
+rqmc_status rqmc_profile_read(rqmc_plan_t p, int* runs, double* ms_gen, double* ms_coarse,
+                              double* ms_fine, double* ms_reduce);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RQMC_H */

@@ -57,6 +57,8 @@ def lib():
         _lib.orc_neumaier.argtypes = [dp, C.c_int64]
         _lib.orc_f_rows.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, i64p, C.c_int64, dp, dp, C.c_int]
         _lib.orc_f_rows_meanid.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, i64p, C.c_int64, dp, C.c_int]
+        _lib.orc_points_rows.argtypes = [C.POINTER(_Prob), i64p, C.c_int64, dp, C.c_int]
+        _lib.orc_f_all_meanid_tab.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, C.c_int]
     return _lib
 
 
@@ -90,6 +92,15 @@ def points(prob, k0: int = 0, n: int | None = None):
     T = np.empty((n, prob.s), dtype=np.uint64)
     lib().orc_points(C.byref(h.s), k0, n, _ptr(X, C.c_double), _ptr(T, C.c_uint64))
     return X, T
+
+
+def points_rows(prob, ks, nthreads: int = 0) -> np.ndarray:
+    """Rows ks (any order) of the point matrix X."""
+    h = _Holder(prob)
+    ks = np.ascontiguousarray(np.asarray(ks, dtype=np.int64))
+    X = np.empty((len(ks), prob.s), dtype=np.float64)
+    lib().orc_points_rows(C.byref(h.s), _ptr(ks, C.c_int64), len(ks), _ptr(X, C.c_double), nthreads)
+    return X
 
 
 def product(X: np.ndarray, A: np.ndarray) -> np.ndarray:
@@ -140,6 +151,17 @@ def f_rows_meanid(prob, ks, nthreads: int = 0):
     if lib().orc_f_rows_meanid(C.byref(h.s), _ptr(A, C.c_double), prob.tau, prob.f,
                                _ptr(ks, C.c_int64), len(ks), _ptr(fk, C.c_double), nthreads):
         raise ValueError("mean identity needs g = id (f in {EXP_MEAN, MEAN})")
+    return fk
+
+
+def f_all_meanid_tab(prob, nthreads: int = 0) -> np.ndarray:
+    """O3' over all N rows with column tabulation (g = id only); returns f_k for k = 0..N-1."""
+    h = _Holder(prob)
+    A = np.ascontiguousarray(prob.A, dtype=np.float64)
+    fk = np.empty(prob.N)
+    err = lib().orc_f_all_meanid_tab(C.byref(h.s), _ptr(A, C.c_double), prob.tau, prob.f, _ptr(fk, C.c_double), nthreads)
+    if err:
+        raise ValueError("mean identity needs g = id" if err == 1 else "allocation failed")
     return fk
 
 

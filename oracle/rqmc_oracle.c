@@ -77,54 +77,71 @@ static double orc_map(const orc_problem* p, double u, int shifted) {
   return orc_invnorm(u);
 }
 
+/* O1 for one entry: coordinate j of point k (value, and its integer word in *word). */
+double orc_point(const orc_problem* p, uint64_t k, int j, uint64_t* word_out) {
+  const uint64_t N = ipow((uint64_t)p->b, p->m);
+  int wj = p->w[j];
+  double u;
+  uint64_t word;
+  int shifted;
+  if (p->kind == 0) {
+    /* z_j = b^{w_j} z'_j; for w_j >= m, z_j is a multiple of N. */
+    uint64_t zj = wj >= p->m ? 0 : (uint64_t)(((unsigned __int128)ipow((uint64_t)p->b, wj) * p->z[j]) % N);
+    word = (uint64_t)(((unsigned __int128)k * zj) % N);     /* k z_j mod N */
+    u = (double)word / (double)N;                            /* { k z_j / N } */
+    shifted = p->shift != NULL;
+    if (shifted) {                                           /* psi(x) = {x + Delta}, reading C-6 */
+      u = u + p->shift[j];
+      if (u >= 1.0) u = u - 1.0;
+    }
+  } else {
+    /* digits of k, least significant first; Chat rows p > m - min(w_j,m) zeroed */
+    int keep_rows = p->m - (wj < p->m ? wj : p->m);
+    uint64_t W = 0;
+    for (int pp = 1; pp <= p->m; ++pp) {            /* output digit p (weight b^-p) */
+      if (pp > keep_rows) continue;                 /* row of Chat is zero */
+      unsigned y = 0;
+      for (int qq = 1; qq <= p->m; ++qq) {          /* input digit q */
+        unsigned kappa = (unsigned)((k >> (qq - 1)) & 1u);
+        unsigned c = (unsigned)((p->C[(size_t)j * p->m + (qq - 1)] >> (p->m - pp)) & 1u);
+        y = (y + c * kappa) % 2u;
+      }
+      W += (uint64_t)y << (p->m - pp);              /* sum_p y_p 2^{m-p} */
+    }
+    shifted = p->dshift != NULL;
+    if (shifted) {
+      word = (W << (53 - p->m)) ^ p->dshift[j];
+      u = (double)word * ldexp(1.0, -53);
+    } else {
+      word = W;
+      u = (double)W * ldexp(1.0, -p->m);
+    }
+  }
+  if (word_out) *word_out = word;
+  return orc_map(p, u, shifted);
+}
+
 /* O1: rows k in [k0, k0+n) of X (row-major n x s); T gets the integer word of each entry:
  * lattice: (k z_j mod N) (numerator over N); net: W (unshifted m-digit word) or V (shifted 53-digit). */
 int orc_points(const orc_problem* p, int64_t k0, int64_t n, double* X, uint64_t* T) {
-  const uint64_t N = ipow((uint64_t)p->b, p->m);
-  for (int64_t i = 0; i < n; ++i) {
-    uint64_t k = (uint64_t)(k0 + i);
+  for (int64_t i = 0; i < n; ++i)
     for (int j = 0; j < p->s; ++j) {
-      int wj = p->w[j];
-      double u;
       uint64_t word;
-      int shifted;
-      if (p->kind == 0) {
-        /* z_j = b^{w_j} z'_j; for w_j >= m, z_j is a multiple of N. */
-        uint64_t zj = wj >= p->m ? 0 : (uint64_t)(((unsigned __int128)ipow((uint64_t)p->b, wj) * p->z[j]) % N);
-        word = (uint64_t)(((unsigned __int128)k * zj) % N);     /* k z_j mod N */
-        u = (double)word / (double)N;                            /* { k z_j / N } */
-        shifted = p->shift != NULL;
-        if (shifted) {                                           /* psi(x) = {x + Delta}, reading C-6 */
-          u = u + p->shift[j];
-          if (u >= 1.0) u = u - 1.0;
-        }
-      } else {
-        /* digits of k, least significant first; Chat rows p > m - min(w_j,m) zeroed */
-        int keep_rows = p->m - (wj < p->m ? wj : p->m);
-        uint64_t W = 0;
-        for (int pp = 1; pp <= p->m; ++pp) {            /* output digit p (weight b^-p) */
-          if (pp > keep_rows) continue;                 /* row of Chat is zero */
-          unsigned y = 0;
-          for (int qq = 1; qq <= p->m; ++qq) {          /* input digit q */
-            unsigned kappa = (unsigned)((k >> (qq - 1)) & 1u);
-            unsigned c = (unsigned)((p->C[(size_t)j * p->m + (qq - 1)] >> (p->m - pp)) & 1u);
-            y = (y + c * kappa) % 2u;
-          }
-          W += (uint64_t)y << (p->m - pp);              /* sum_p y_p 2^{m-p} */
-        }
-        shifted = p->dshift != NULL;
-        if (shifted) {
-          word = (W << (53 - p->m)) ^ p->dshift[j];
-          u = (double)word * ldexp(1.0, -53);
-        } else {
-          word = W;
-          u = (double)W * ldexp(1.0, -p->m);
-        }
-      }
+      double x = orc_point(p, (uint64_t)(k0 + i), j, &word);
       if (T) T[i * p->s + j] = word;
-      if (X) X[i * p->s + j] = orc_map(p, u, shifted);
+      if (X) X[i * p->s + j] = x;
     }
-  }
+  return 0;
+}
+
+/* O1 on arbitrary rows ks[0..n): X (n x s). */
+int orc_points_rows(const orc_problem* p, const int64_t* ks, int64_t n, double* X, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < p->s; ++j) X[i * p->s + j] = orc_point(p, (uint64_t)ks[i], j, NULL);
   return 0;
 }
 
@@ -223,5 +240,41 @@ int orc_f_rows_meanid(const orc_problem* p, const double* A, int tau, int f, con
     free(x);
   }
   free(abar);
+  return 0;
+}
+
+/* O3' over ALL rows with the column tabulation SURVEY §8(c) allows: x_{k,j} depends only on
+ * k mod M_j (pinned by the periodicity tests), so column j is tabulated from its plain
+ * definition at k = 0..M_j-1 and f_k = F(sum_j tab_j[k mod M_j] abar_j) (increasing j). */
+int orc_f_all_meanid_tab(const orc_problem* p, const double* A, int tau, int f, double* fk, int nthreads) {
+  if (f != 0 && f != 3) return 1;
+  const uint64_t N = ipow((uint64_t)p->b, p->m);
+  uint64_t* M = (uint64_t*)malloc(sizeof(uint64_t) * p->s);
+  size_t* off = (size_t*)malloc(sizeof(size_t) * (p->s + 1));
+  double* abar = (double*)malloc(sizeof(double) * p->s);
+  off[0] = 0;
+  for (int j = 0; j < p->s; ++j) {
+    int wj = p->w[j] < p->m ? p->w[j] : p->m;
+    M[j] = ipow((uint64_t)p->b, p->m - wj);
+    off[j + 1] = off[j] + M[j];
+    double acc = 0.0;
+    for (int c = 0; c < tau; ++c) acc = acc + A[(size_t)j * tau + c];
+    abar[j] = acc / tau;
+  }
+  double* tab = (double*)malloc(sizeof(double) * off[p->s]);
+  if (!tab) { free(M); free(off); free(abar); return 2; }
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int j = 0; j < p->s; ++j)
+    for (uint64_t r = 0; r < M[j]; ++r) tab[off[j] + r] = orc_point(p, r, j, NULL);
+#pragma omp parallel for schedule(static, 4096)
+  for (int64_t k = 0; k < (int64_t)N; ++k) {
+    double acc = 0.0;
+    for (int j = 0; j < p->s; ++j) acc = acc + tab[off[j] + (uint64_t)k % M[j]] * abar[j];
+    fk[k] = f == 0 ? exp(acc) : acc;
+  }
+  free(tab); free(M); free(off); free(abar);
   return 0;
 }

@@ -1,0 +1,71 @@
+// Internal interface between the host planner (rqmc_plan.cpp) and the sm_100a kernels
+// (rqmc_kernels.cu).  Not part of the public C ABI (include/rqmc.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace rqmc {
+
+constexpr int kMaxLevels = 64;
+constexpr int kMaxFine = 8;       // fused fine levels (compile-time DFS depth)
+constexpr int kBundle = 32;       // residues of the checkpoint level per fine CTA
+constexpr int kFineBN = 64;       // column tile of the fine kernel
+constexpr int kFineThreads = 256;
+
+// Point-generation view of one level (local rows r'' of this rank).
+struct GenLevel {
+  int64_t M;      // global distinct rows b^{m-w}
+  int64_t Ml;     // local rows
+  int64_t xoff;   // offset (doubles) of X^red in the workspace
+  int j_lo, s_w, ldx, pad;
+};
+
+struct GenArgs {
+  int kind, map, b, m, shifted, rank, world, nlev;
+  double zero_u;                 // u substituted for 0 under Phi^-1 (reading C-5)
+  const uint64_t* z;             // lattice z'_j
+  const double* shift;           // lattice Delta_j
+  const uint64_t* C;             // net column words (row-zeroed)
+  const uint64_t* dshift;        // net sigma_j
+  double* X;                     // workspace base
+  GenLevel lv[kMaxLevels];
+};
+
+struct GemmArgs {                // one coarse level: R = tile(Rp) + X A_w
+  const double* X; int64_t ldx;
+  int64_t M;                     // local rows of this level
+  int K;                         // s_w
+  const double* A; int64_t lda;  // A + j_lo * lda
+  int tau;
+  const double* Rp; int64_t ldp; int64_t Mp;   // parent R (nullptr: zero)
+  double* R; int64_t ldr;
+};
+
+struct FineLevel {
+  const double* X; int ldx; int K; int j_lo; int fan; int runs; int xs_off; int as_off;
+};
+
+struct FineArgs {
+  const double* root; int64_t ldroot; int64_t Mroot;
+  int NF;
+  FineLevel lv[kMaxFine];
+  const double* A; int64_t lda; int tau; int a_vec;  // a_vec: 16B cp.async allowed
+  double* Y; int64_t ldy; int y_vec;  // y_vec: 16B stores allowed
+  int fk; double fp0, fp1;
+  double* partial;
+  int leafruns;
+  int as_stride;      // doubles per A buffer
+  int acc_off;        // rowacc offset (doubles)
+  int smem_bytes;
+};
+
+cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, cudaStream_t st);
+cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, uint64_t* words,
+                          double* vals, cudaStream_t st);
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, cudaStream_t st);
+cudaError_t launch_reduce(const double* partial, int64_t n, double* out, cudaStream_t st);
+
+}  // namespace rqmc

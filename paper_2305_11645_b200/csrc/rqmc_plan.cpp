@@ -1,0 +1,554 @@
+// Host side of the C ABI (include/rqmc.h): validation, the level planner,
+// workspace layout and the launch sequence of one run.  No arithmetic of the product lives here.
+//
+// Level planner: levels w = min(w_j, m) are contiguous j-ranges because w is
+// nondecreasing; s* = max{j : w_j < m} drops the zero columns j > s*
+// unless a shift or the Phi^-1 map makes them a constant row (reading C-4, kept as a 1-row level m).
+// Each non-empty level's parent is the next coarser non-empty level w' (tile factor b^{w'-w},
+// reading C-3).  A checkpoint level splits the table into coarse levels (one DMMA GEMM launch each,
+// R materialised in the workspace) and <= 8 fine levels fused into k_fine.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rqmc.h"
+#include "rqmc_internal.h"
+
+using namespace rqmc;
+
+namespace {
+
+struct Level {
+  int w, j_lo, s_w, parent, coarse;
+  int64_t M, Ml;
+  int ldx;
+  int64_t xoff;   // doubles
+  int rbuf;       // coarse: which R buffer
+};
+
+int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+bool is_prime(int b) {
+  if (b < 2) return false;
+  for (int d = 2; (int64_t)d * d <= b; ++d)
+    if (b % d == 0) return false;
+  return true;
+}
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) { int64_t t = a % b; a = b; b = t; }
+  return a;
+}
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct rqmc_plan_s {
+  int b = 0, m = 0, s = 0, tau = 0, kind = 0, map = 0, rank = 0, world = 1;
+  bool shifted = false;
+  int64_t N = 0, Nl = 0;
+  int s_star = 0;
+  std::vector<int32_t> w;
+  std::vector<uint64_t> z, C, dshift;
+  std::vector<double> shift;
+  std::vector<Level> lv;     // coarse -> fine
+  int ckpt = 0, nfine = 0;
+  int64_t nbundles = 0;
+  int ldr = 0;               // row stride of R buffers
+  size_t off_x = 0, off_r[2] = {0, 0}, off_part = 0, off_a = 0, off_fsum = 0, total = 0;
+  int64_t max_gen_entries = 0;
+  // fine-kernel shared-memory layout
+  int fine_smem = 0, fine_as_stride = 0, fine_acc_off = 0, leafruns = 1;
+  std::vector<int> fine_xs_off, fine_as_off;
+  // device tables (uploaded once, lazily)
+  std::once_flag up_once;
+  cudaError_t up_err = cudaSuccess;
+  uint64_t* d_z = nullptr;
+  double* d_shift = nullptr;
+  uint64_t* d_C = nullptr;
+  uint64_t* d_ds = nullptr;
+  // phase profiling: 5 events per recorded run
+  std::vector<cudaEvent_t> prof_ev;
+  int prof_max = 0, prof_runs = 0;
+  std::string err;
+};
+
+namespace {
+
+rqmc_status fail(rqmc_plan_s* p, rqmc_status st, const std::string& msg) {
+  if (p) p->err = msg;
+  return st;
+}
+
+thread_local std::string g_create_err;
+
+// Shared-memory bytes of the fine kernel when the checkpoint is level index c.
+int fine_smem_bytes(const rqmc_plan_s& p, int c, std::vector<int>* xs_off, std::vector<int>* as_off,
+                    int* as_stride, int* acc_off, int* leafruns) {
+  const int nl = (int)p.lv.size();
+  size_t xs = 0, as = 0;
+  if (xs_off) xs_off->clear();
+  if (as_off) as_off->clear();
+  const int64_t Mroot = p.lv[c].Ml;
+  int lr = 1;
+  for (int i = c + 1; i < nl; ++i) {
+    const int64_t runs = p.lv[i].Ml / Mroot;
+    if (xs_off) xs_off->push_back((int)xs);
+    if (as_off) as_off->push_back((int)as);
+    xs += (size_t)runs * p.lv[i].s_w * kBundle;
+    as += (size_t)p.lv[i].s_w * kFineBN;
+    lr = (int)runs;
+  }
+  xs = align_up(xs, 2);
+  as = align_up(as, 2);
+  const size_t acc = 2 * (size_t)lr * kBundle;
+  // layout: [A buf 0][A buf 1][X subtree][rowacc]
+  if (as_stride) *as_stride = (int)as;
+  if (xs_off)
+    for (auto& o : *xs_off) o += (int)(2 * as);
+  if (acc_off) *acc_off = (int)(2 * as + xs);
+  if (leafruns) *leafruns = lr;
+  return (int)((2 * as + xs + acc) * sizeof(double));
+}
+
+constexpr int kFineSmemLimit = 200 * 1024;
+
+}  // namespace
+
+extern "C" {
+
+const char* rqmc_strerror(rqmc_status s) {
+  switch (s) {
+    case RQMC_OK: return "ok";
+    case RQMC_EINVAL: return "invalid argument";
+    case RQMC_ENOTPRIME: return "base b is not prime";
+    case RQMC_EWORDER: return "reduction indices must be nondecreasing with w_1 = 0";
+    case RQMC_EZUNIT: return "generating vector component is not a unit mod b^(m-w_j)";
+    case RQMC_ESHIFT: return "shift outside [0,1) (or digital shift >= 2^53)";
+    case RQMC_ENETMAT: return "invalid or non-periodic digital net generating matrices";
+    case RQMC_EDIM: return "dimension mismatch";
+    case RQMC_EDOMAIN: return "inverse normal domain error";
+    case RQMC_ECUDA: return "CUDA error";
+    case RQMC_ENOMEM: return "out of memory";
+    case RQMC_EUNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* rqmc_plan_last_error(rqmc_plan_t p) { return p ? p->err.c_str() : g_create_err.c_str(); }
+
+rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
+  g_create_err.clear();
+  if (!d || !out) return RQMC_EINVAL;
+  *out = nullptr;
+  auto bad = [&](rqmc_status st, const std::string& m) { g_create_err = m; return st; };
+  if (d->m < 1 || d->s < 1 || d->tau < 1) return bad(RQMC_EDIM, "m, s, tau must be >= 1");
+  if (!is_prime(d->b)) return bad(RQMC_ENOTPRIME, "b = " + std::to_string(d->b) + " is not prime");
+  if (!d->w) return bad(RQMC_EINVAL, "w is NULL");
+  if (d->kind != RQMC_LATTICE && d->kind != RQMC_DIGITAL_NET) return bad(RQMC_EINVAL, "bad kind");
+  if (d->map != RQMC_MAP_UNIT && d->map != RQMC_MAP_INVNORM) return bad(RQMC_EINVAL, "bad map");
+  if (d->m * std::log2((double)d->b) > 32.0 + 1e-9) return bad(RQMC_EUNSUPPORTED, "N = b^m > 2^32");
+  if (d->kind == RQMC_DIGITAL_NET && (d->b != 2 || d->m > 32))
+    return bad(RQMC_EUNSUPPORTED, "digital nets need b = 2, m <= 32");
+  if (d->w[0] != 0) return bad(RQMC_EWORDER, "w_1 != 0 (P:284)");
+  for (int j = 1; j < d->s; ++j)
+    if (d->w[j] < d->w[j - 1])
+      return bad(RQMC_EWORDER, "w decreases at j = " + std::to_string(j + 1));
+
+  auto* p = new rqmc_plan_s();
+  p->b = d->b; p->m = d->m; p->s = d->s; p->tau = d->tau; p->kind = d->kind; p->map = d->map;
+  p->N = ipow(d->b, d->m);
+  p->world = d->world <= 0 ? 1 : d->world;
+  p->rank = d->rank;
+  {  // world must be a power of b dividing N
+    int64_t g = p->world;
+    while (g > 1 && g % p->b == 0) g /= p->b;
+    if (g != 1 || p->N % p->world != 0 || p->rank < 0 || p->rank >= p->world) {
+      delete p;
+      return bad(RQMC_EUNSUPPORTED, "world must be a power of b dividing N and 0 <= rank < world");
+    }
+  }
+  p->Nl = p->N / p->world;
+  p->w.assign(d->w, d->w + d->s);
+  p->s_star = 0;
+  for (int j = 0; j < d->s; ++j)
+    if (d->w[j] < d->m) p->s_star = j + 1;
+
+  if (d->kind == RQMC_LATTICE) {
+    if (!d->z) { delete p; return bad(RQMC_EINVAL, "z is NULL"); }
+    p->z.assign(d->z, d->z + d->s);
+    for (int j = 0; j < d->s; ++j) {
+      const int wj = std::min<int>(d->w[j], d->m);
+      const int64_t Mj = ipow(d->b, d->m - wj);
+      const uint64_t zj = d->z[j];
+      const bool ok = (Mj == 1) ? (zj == 1) : (zj >= 1 && zj < (uint64_t)Mj && gcd64((int64_t)zj, d->b) == 1);
+      if (!ok) {
+        delete p;
+        return bad(RQMC_EZUNIT, "z'_" + std::to_string(j + 1) + " = " + std::to_string(zj) +
+                                    " not in U_{b^{m-w_j}} (P:287-292)");
+      }
+    }
+    if (d->shift) {
+      p->shifted = true;
+      p->shift.assign(d->shift, d->shift + d->s);
+      for (int j = 0; j < d->s; ++j)
+        if (!(d->shift[j] >= 0.0 && d->shift[j] < 1.0)) {
+          delete p;
+          return bad(RQMC_ESHIFT, "shift_" + std::to_string(j + 1) + " outside [0,1)");
+        }
+    }
+  } else {
+    if (!d->C) { delete p; return bad(RQMC_EINVAL, "C is NULL"); }
+    p->C.assign(d->C, d->C + (size_t)d->s * d->m);
+    for (int j = 0; j < d->s; ++j) {
+      const int wj = std::min<int>(d->w[j], d->m);
+      const uint64_t low = wj >= 64 ? ~0ull : ((1ull << wj) - 1);  // rows p > m - w_j <-> bits < w_j
+      for (int q = 0; q < d->m; ++q) {
+        uint64_t& col = p->C[(size_t)j * d->m + q];
+        if (col >> d->m) {
+          delete p;
+          return bad(RQMC_ENETMAT, "column word j=" + std::to_string(j + 1) + " q=" + std::to_string(q) + " >= 2^m");
+        }
+        col &= ~low;  // Eq. reduced_genmat_net2: zero the last min(w_j,m) rows
+        if (q >= d->m - wj && col != 0) {
+          delete p;
+          return bad(RQMC_ENETMAT, "reduced net coordinate j=" + std::to_string(j + 1) +
+                                       " depends on digit " + std::to_string(q) +
+                                       " >= m - w_j: not periodic; Alg. 2 needs column deletion (P:671)");
+        }
+      }
+    }
+    if (d->dshift) {
+      p->shifted = true;
+      p->dshift.assign(d->dshift, d->dshift + d->s);
+      for (int j = 0; j < d->s; ++j)
+        if (d->dshift[j] >> 53) {
+          delete p;
+          return bad(RQMC_ESHIFT, "digital shift_" + std::to_string(j + 1) + " >= 2^53");
+        }
+    }
+  }
+
+  // ---- level table (coarse -> fine) ----
+  {
+    std::vector<Level> fine_to_coarse;
+    int j = 0;
+    while (j < d->s) {
+      const int wl = std::min<int>(d->w[j], d->m);
+      int j2 = j;
+      while (j2 < d->s && std::min<int>(d->w[j2], d->m) == wl) ++j2;
+      // columns j > s* are x = 0: dropped, unless a shift or the map makes them the
+      // constant phi_j(Delta_j) / Phi^-1(zero rule) -- then a 1-row level m (reading C-4)
+      if (wl < d->m || p->shifted || d->map != RQMC_MAP_UNIT) {
+        Level L{};
+        L.w = wl; L.j_lo = j; L.s_w = j2 - j;
+        L.M = ipow(d->b, d->m - wl);
+        L.Ml = L.M >= p->world ? L.M / p->world : 1;
+        fine_to_coarse.push_back(L);
+      }
+      j = j2;
+    }
+    p->lv.assign(fine_to_coarse.rbegin(), fine_to_coarse.rend());
+    for (size_t i = 0; i < p->lv.size(); ++i) p->lv[i].parent = (int)i - 1;
+  }
+  const int nl = (int)p->lv.size();
+
+  // ---- checkpoint choice: most fused fine levels subject to depth <= 8, smem, and >= 2 waves ----
+  {
+    int best = -1;
+    for (int c = 0; c < nl; ++c) {
+      const int nf = nl - 1 - c;
+      if (nf > kMaxFine) continue;
+      if (fine_smem_bytes(*p, c, nullptr, nullptr, nullptr, nullptr, nullptr) > kFineSmemLimit) continue;
+      const int64_t nb = (p->lv[c].Ml + kBundle - 1) / kBundle;
+      if (best < 0) best = c;
+      if (nb >= 2 * 148) { best = c; break; }
+      best = c;  // keep moving finer while parallelism is insufficient
+    }
+    if (const char* env = std::getenv("RQMC_CKPT_W")) {  // tuning override: checkpoint at level w
+      const int wv = std::atoi(env);
+      for (int c = 0; c < nl; ++c)
+        if (p->lv[c].w == wv && nl - 1 - c <= kMaxFine &&
+            fine_smem_bytes(*p, c, nullptr, nullptr, nullptr, nullptr, nullptr) <= kFineSmemLimit)
+          best = c;
+    }
+    if (best < 0) { delete p; return bad(RQMC_EUNSUPPORTED, "no feasible checkpoint level"); }
+    p->ckpt = best;
+    p->nfine = nl - 1 - best;
+    for (int i = 0; i < nl; ++i) p->lv[i].coarse = i <= best;
+    p->nbundles = (p->lv[best].Ml + kBundle - 1) / kBundle;
+    p->fine_smem = fine_smem_bytes(*p, best, &p->fine_xs_off, &p->fine_as_off, &p->fine_as_stride,
+                                   &p->fine_acc_off, &p->leafruns);
+  }
+
+  // ---- workspace layout ----
+  {
+    size_t off = 0;
+    p->off_x = 0;
+    for (auto& L : p->lv) {
+      L.ldx = L.coarse ? (L.s_w + 1) / 2 * 2 : L.s_w;
+      L.xoff = (int64_t)(off / sizeof(double));
+      off = align_up(off + (size_t)L.Ml * L.ldx * sizeof(double), 256);
+      p->max_gen_entries = std::max<int64_t>(p->max_gen_entries, L.Ml * L.ldx);
+    }
+    p->ldr = (p->tau + 1) / 2 * 2;
+    size_t rsz[2] = {0, 0};
+    for (int i = 0; i <= p->ckpt; ++i) {
+      p->lv[i].rbuf = i & 1;
+      rsz[i & 1] = std::max(rsz[i & 1], (size_t)p->lv[i].Ml * p->ldr * sizeof(double));
+    }
+    p->off_r[0] = off; off = align_up(off + rsz[0], 256);
+    p->off_r[1] = off; off = align_up(off + rsz[1], 256);
+    p->off_part = off; off = align_up(off + (size_t)p->nbundles * sizeof(double), 256);
+    p->off_fsum = off; off = align_up(off + sizeof(double), 256);
+    p->off_a = off; off = align_up(off + (size_t)p->s * p->ldr * sizeof(double), 256);
+    p->total = off;
+  }
+  *out = p;
+  return RQMC_OK;
+}
+
+void rqmc_plan_destroy(rqmc_plan_t p) {
+  if (!p) return;
+  for (auto e : p->prof_ev) cudaEventDestroy(e);
+  if (p->d_z) cudaFree(p->d_z);
+  if (p->d_shift) cudaFree(p->d_shift);
+  if (p->d_C) cudaFree(p->d_C);
+  if (p->d_ds) cudaFree(p->d_ds);
+  delete p;
+}
+
+rqmc_status rqmc_plan_summary_get(rqmc_plan_t p, rqmc_plan_summary* o) {
+  if (!p || !o) return RQMC_EINVAL;
+  o->n_levels = (int)p->lv.size();
+  o->checkpoint = p->ckpt;
+  o->n_fine = p->nfine;
+  o->n_bundles = p->nbundles;
+  o->N_local = p->Nl;
+  o->s_star = p->s_star;
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* o) {
+  if (!p || !o || idx < 0 || idx >= (int)p->lv.size()) return RQMC_EINVAL;
+  const Level& L = p->lv[idx];
+  o->w = L.w; o->j_lo = L.j_lo; o->s_w = L.s_w; o->M = L.M; o->M_local = L.Ml;
+  o->parent = L.parent; o->coarse = L.coarse;
+  return RQMC_OK;
+}
+
+int64_t rqmc_plan_global_row(rqmc_plan_t p, int64_t i) { return p ? p->rank + (int64_t)p->world * i : -1; }
+
+rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* rows, double* macs, double* bytes) {
+  if (!p) return RQMC_EINVAL;
+  double mac = 0.0;
+  for (auto& L : p->lv) mac += (double)L.Ml * L.s_w * p->tau;  // tau sum_w M_w s_w
+  if (rows) *rows = p->Nl;
+  if (macs) *macs = mac;
+  if (bytes) *bytes = 8.0 * p->s * p->tau + (want_y ? 8.0 * p->Nl * p->tau : 0.0);
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_workspace_size(rqmc_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return RQMC_EINVAL;
+  *bytes = p->total;
+  return RQMC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+rqmc_status upload(rqmc_plan_s* p) {
+  std::call_once(p->up_once, [p]() {
+    auto cp = [&](auto& dst, const auto& src) {
+      if (src.empty() || p->up_err != cudaSuccess) return;
+      const size_t n = src.size() * sizeof(src[0]);
+      p->up_err = cudaMalloc((void**)&dst, n);
+      if (p->up_err == cudaSuccess) p->up_err = cudaMemcpy(dst, src.data(), n, cudaMemcpyHostToDevice);
+    };
+    cp(p->d_z, p->z);
+    cp(p->d_shift, p->shift);
+    cp(p->d_C, p->C);
+    cp(p->d_ds, p->dshift);
+  });
+  if (p->up_err != cudaSuccess)
+    return fail(p, RQMC_ECUDA, std::string("device table upload: ") + cudaGetErrorString(p->up_err));
+  return RQMC_OK;
+}
+
+GenArgs gen_args(const rqmc_plan_s* p, void* work) {
+  GenArgs g{};
+  g.kind = p->kind; g.map = p->map; g.b = p->b; g.m = p->m; g.shifted = p->shifted;
+  g.rank = p->rank; g.world = p->world; g.nlev = (int)p->lv.size();
+  g.zero_u = p->shifted ? std::ldexp(1.0, -53) : 0.5 / (double)p->N;
+  g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds;
+  g.X = reinterpret_cast<double*>(static_cast<char*>(work) + p->off_x);
+  for (size_t i = 0; i < p->lv.size(); ++i) {
+    const Level& L = p->lv[i];
+    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, 0};
+  }
+  return g;
+}
+
+rqmc_status check_cuda(rqmc_plan_s* p, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RQMC_OK;
+  return fail(p, RQMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                const double* fparam, double* d_fsum, void* dwork, size_t wbytes, cudaStream_t st) {
+  if (!p || !dA || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->total));
+  if (lda < p->tau || (dY && ldy < p->tau)) return fail(p, RQMC_EDIM, "lda/ldy < tau");
+  if (f < RQMC_F_NONE || f > RQMC_F_MEAN) return fail(p, RQMC_EINVAL, "bad f");
+  if (f == RQMC_F_CALL_MEAN_EXP && !fparam) return fail(p, RQMC_EINVAL, "f needs fparam");
+  const bool want_f = f != RQMC_F_NONE && d_fsum;
+  if (!want_f && !dY) return RQMC_OK;
+  if (rqmc_status s = upload(p)) return s;
+  char* w = static_cast<char*>(dwork);
+  cudaEvent_t* ev = nullptr;
+  if (p->prof_runs < p->prof_max) ev = &p->prof_ev[5 * p->prof_runs++];
+  auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
+  mark(0);
+
+  // a2: reduced points of every level
+  GenArgs g = gen_args(p, dwork);
+  if (rqmc_status s = check_cuda(p, launch_gen(g, p->max_gen_entries, st), "k_gen")) return s;
+  mark(1);
+
+  // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine
+  for (int i = 0; i <= p->ckpt; ++i) {
+    const Level& L = p->lv[i];
+    GemmArgs a{};
+    a.X = g.X + L.xoff; a.ldx = L.ldx; a.M = L.Ml; a.K = L.s_w;
+    a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda; a.tau = p->tau;
+    if (L.parent >= 0) {
+      const Level& P = p->lv[L.parent];
+      a.Rp = reinterpret_cast<const double*>(w + p->off_r[P.rbuf]); a.ldp = p->ldr; a.Mp = P.Ml;
+    }
+    a.R = reinterpret_cast<double*>(w + p->off_r[L.rbuf]); a.ldr = p->ldr;
+    if (rqmc_status s = check_cuda(p, launch_gemm(a, st), "k_level_gemm")) return s;
+  }
+
+  mark(2);
+
+  // a3+a4+a5 fine levels fused with f / Y store
+  FineArgs fa{};
+  const Level& R = p->lv[p->ckpt];
+  fa.root = reinterpret_cast<const double*>(w + p->off_r[R.rbuf]); fa.ldroot = p->ldr; fa.Mroot = R.Ml;
+  fa.NF = p->nfine;
+  for (int i = 0; i < p->nfine; ++i) {
+    const Level& L = p->lv[p->ckpt + 1 + i];
+    FineLevel& F = fa.lv[i];
+    F.X = g.X + L.xoff; F.ldx = L.ldx; F.K = L.s_w; F.j_lo = L.j_lo;
+    F.runs = (int)(L.Ml / R.Ml);
+    F.fan = i == 0 ? F.runs : F.runs / fa.lv[i - 1].runs;
+    F.xs_off = p->fine_xs_off[i]; F.as_off = p->fine_as_off[i];
+  }
+  fa.A = dA; fa.lda = lda; fa.tau = p->tau;
+  fa.a_vec = ((uintptr_t)dA % 16 == 0) && (lda % 2 == 0) && (p->tau % 2 == 0);
+  fa.Y = dY; fa.ldy = ldy;
+  fa.y_vec = ((uintptr_t)dY % 16 == 0) && (ldy % 2 == 0);
+  fa.fk = want_f ? (int)f : -1;
+  fa.fp0 = fparam ? fparam[0] : 0.0;
+  fa.fp1 = fparam ? fparam[1] : 0.0;
+  fa.partial = reinterpret_cast<double*>(w + p->off_part);
+  fa.leafruns = p->leafruns;
+  fa.as_stride = p->fine_as_stride;
+  fa.acc_off = p->fine_acc_off;
+  fa.smem_bytes = p->fine_smem;
+  if (rqmc_status s = check_cuda(p, launch_fine(fa, p->nbundles, st), "k_fine")) return s;
+  mark(3);
+  if (want_f)
+    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, p->nbundles, d_fsum, st), "k_reduce")) return s;
+  mark(4);
+  return RQMC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rqmc_status rqmc_xa(rqmc_plan_t p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                    const double* fparam, double* d_fsum, void* dwork, size_t wbytes, void* stream) {
+  return run(p, dA, lda, dY, ldy, f, fparam, d_fsum, dwork, wbytes, static_cast<cudaStream_t>(stream));
+}
+
+rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, const double* fparam,
+                    double* d_fsum, void* dwork, size_t wbytes, void* stream) {
+  if (!d_fsum || f == RQMC_F_NONE) return fail(p, RQMC_EINVAL, "rqmc_qn needs f and d_fsum");
+  return run(p, dA, lda, nullptr, 0, f, fparam, d_fsum, dwork, wbytes, static_cast<cudaStream_t>(stream));
+}
+
+rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
+                         double* h_fsum, void* dwork, size_t wbytes, void* stream) {
+  if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small");
+  if (lda < p->tau) return fail(p, RQMC_EDIM, "lda < tau");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(dwork);
+  double* dA = reinterpret_cast<double*>(w + p->off_a);
+  double* dsum = reinterpret_cast<double*>(w + p->off_fsum);
+  cudaError_t e = cudaMemcpy2DAsync(dA, (size_t)p->ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
+                                    (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, st);
+  if (rqmc_status s = check_cuda(p, e, "H2D A")) return s;
+  if (rqmc_status s = rqmc_qn(p, dA, p->ldr, f, fparam, dsum, dwork, wbytes, stream)) return s;
+  e = cudaMemcpyAsync(h_fsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return check_cuda(p, e, "D2H fsum");
+}
+
+rqmc_status rqmc_points(rqmc_plan_t p, int idx, int64_t r0, int64_t count, uint64_t* d_words, double* d_vals,
+                        void* stream) {
+  if (!p || idx < 0 || idx >= (int)p->lv.size() || r0 < 0 || count < 0 || r0 + count > p->lv[idx].Ml)
+    return fail(p, RQMC_EINVAL, "bad level / row range");
+  if (rqmc_status s = upload(p)) return s;
+  GenArgs g = gen_args(p, nullptr);
+  return check_cuda(p, launch_points(g, idx, r0, count, d_words, d_vals, static_cast<cudaStream_t>(stream)),
+                    "k_points");
+}
+
+rqmc_status rqmc_profile_enable(rqmc_plan_t p, int max_runs) {
+  if (!p || max_runs < 0) return RQMC_EINVAL;
+  for (auto e : p->prof_ev) cudaEventDestroy(e);
+  p->prof_ev.clear();
+  p->prof_runs = 0;
+  p->prof_max = 0;
+  if (max_runs == 0) return RQMC_OK;
+  p->prof_ev.resize((size_t)5 * max_runs);
+  for (auto& e : p->prof_ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return fail(p, RQMC_ECUDA, "cudaEventCreate");
+  p->prof_max = max_runs;
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_profile_read(rqmc_plan_t p, int* runs, double* ms_gen, double* ms_coarse, double* ms_fine,
+                              double* ms_reduce) {
+  if (!p) return RQMC_EINVAL;
+  double acc[4] = {0, 0, 0, 0};
+  for (int r = 0; r < p->prof_runs; ++r) {
+    cudaEvent_t* ev = &p->prof_ev[5 * r];
+    if (cudaEventSynchronize(ev[4]) != cudaSuccess) return fail(p, RQMC_ECUDA, "cudaEventSynchronize");
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) != cudaSuccess) return fail(p, RQMC_ECUDA, "elapsed");
+      acc[i] += ms;
+    }
+  }
+  if (runs) *runs = p->prof_runs;
+  if (ms_gen) *ms_gen = acc[0];
+  if (ms_coarse) *ms_coarse = acc[1];
+  if (ms_fine) *ms_fine = acc[2];
+  if (ms_reduce) *ms_reduce = acc[3];
+  return RQMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star; SURVEY §8(c) "Tolerances"):
+  * point indices / digit words: bit-exact; unit-map lattice/net values: bit-exact;
+  * Y entries: |Y_gpu - Y_orc| <= 1e-12 * max(1, |x_k|_inf) * |A_{:,c}|_1;
+  * exact-arithmetic regime (b = 2, dyadic shift <= 30 bits, small-integer A): bit-identical;
+  * Q_N: relative 1e-12.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rq():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2305_11645_b200 import _build
+    _build.build()
+    import paper_2305_11645_b200 as rq
+    return rq
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def y_tol(prob, X):
+    """1e-12 * max(1, |x_k|_inf) * |A_c|_1 (rows of X = the points of the compared rows)."""
+    xa = np.maximum(1.0, np.abs(X).max(axis=1))[:, None]
+    return 1e-12 * xa * np.abs(prob.A).sum(axis=0)[None, :]
+
+
+def check_y(prob, Yg, ks):
+    Xs = oracle.points_rows(prob, ks)
+    Yo = oracle.product(Xs, prob.A)
+    err = np.abs(Yg - Yo)
+    tol = y_tol(prob, Xs)
+    bad = err > tol
+    assert not bad.any(), f"max err/tol {np.max(err / tol):.3g} at {np.argwhere(bad)[:3]}"
+    return float(np.max(err / np.maximum(tol, 1e-300)))
+
+
+def run_xa(rq, prob, f=None, **plan_kw):
+    p = rq.Plan.from_problem(prob, **plan_kw)
+    A = dev(prob.A)
+    ff = prob.f if f is None else f
+    Y, fs = p.xa(A, ff, prob.fparam)
+    torch.cuda.synchronize()
+    return p, Y.cpu().numpy(), float(fs.item())
+
+
+# ------------------------------------------------------------------ a2: points
+
+@pytest.mark.parametrize("case", ["lat2", "lat2_shift_invnorm", "lat3_shift_invnorm", "net", "net_shift",
+                                  "lat5_wbig_shift"])
+def test_points_bit_exact(rq, case):
+    if case == "lat2":
+        prob = W.make_random(1, 2, 12, 100, 3)
+    elif case == "lat2_shift_invnorm":
+        prob = W.make_random(2, 2, 12, 100, 3, shifted=True, mapping=W.MAP_INVNORM)
+    elif case == "lat3_shift_invnorm":
+        prob = W.make_random(3, 3, 8, 90, 3, shifted=True, mapping=W.MAP_INVNORM)
+    elif case == "net":
+        prob = W.make_random(4, 2, 12, 100, 3, kind=W.KIND_NET)
+    elif case == "net_shift":
+        prob = W.make_random(5, 2, 12, 100, 3, kind=W.KIND_NET, shifted=True, mapping=W.MAP_INVNORM)
+    else:
+        prob = W.make_random(6, 5, 4, 40, 3, shifted=True, wmode="rand")
+    p = rq.Plan.from_problem(prob)
+    for idx, L in enumerate(p.levels()):
+        words, vals = p.points(idx)
+        words = words.cpu().numpy().view(np.uint64)
+        vals = vals.cpu().numpy()
+        Xo, To = oracle.points(prob, 0, L["M"])        # x_{k,j} depends on k mod M (k = r < M)
+        js = slice(L["j_lo"], L["j_lo"] + L["s_w"])
+        if prob.kind == W.KIND_LATTICE:
+            scale = np.uint64(prob.N // L["M"]) if L["w"] < prob.m else np.uint64(1)
+            exp_words = To[:, js] // scale if L["w"] < prob.m else np.zeros_like(To[:, js])
+        else:
+            exp_words = To[:, js]
+        assert np.array_equal(words, exp_words), f"level {idx} words"
+        if prob.map == W.MAP_UNIT:
+            assert np.array_equal(vals, Xo[:, js]), f"level {idx} values"
+        else:
+            np.testing.assert_allclose(vals, Xo[:, js], rtol=4e-15, atol=4e-15)
+
+
+# ------------------------------------------------------------------ exact regime: bit-identical
+
+@pytest.mark.parametrize("seed,kind,m,s,tau,shifted,ckpt", [
+    (11, W.KIND_LATTICE, 11, 63, 70, False, None),
+    (12, W.KIND_LATTICE, 12, 130, 64, True, None),
+    (13, W.KIND_NET, 11, 70, 33, True, None),
+    (14, W.KIND_LATTICE, 13, 200, 129, True, "4"),
+    (15, W.KIND_LATTICE, 13, 200, 129, True, "0"),
+    (16, W.KIND_NET, 12, 64, 96, False, "7"),
+])
+def test_xa_exact_regime_bit_identical(rq, monkeypatch, seed, kind, m, s, tau, shifted, ckpt):
+    """b=2, dyadic shift, |A| <= 8: every partial sum exact -> GPU == oracle bit for bit
+    (SURVEY §8(c) exact-arithmetic regime); spans several tiles + ragged tails, several checkpoints."""
+    if ckpt is not None:
+        monkeypatch.setenv("RQMC_CKPT_W", ckpt)
+    prob = W.make_random(seed, 2, m, s, tau, kind=kind, shifted=shifted, int_a=True, f=W.F_MEAN)
+    p, Y, fs = run_xa(rq, prob)
+    Yo = oracle.xa(prob)
+    assert np.array_equal(Y, Yo)
+    q = oracle.qn_sum(prob)
+    assert abs(fs - q) <= 1e-12 * max(1.0, abs(q))
+
+
+def test_identity_matrix_returns_points(rq):
+    """A = I_s: XA = X, so the whole path (levels, tiles, stores) returns the points bit-exactly."""
+    prob = W.make_random(21, 2, 10, 48, 48, shifted=True)
+    prob.A = np.eye(48)
+    pl = rq.Plan.from_problem(prob)
+    Yg = pl.xa(dev(prob.A)).cpu().numpy()
+    X, _ = oracle.points(prob)
+    assert np.array_equal(Yg, X)
+
+
+def test_golden_g1_through_gpu(rq):
+    """SURVEY G1 (P:307-309 by hand) through the GPU path, bit-exact."""
+    A = np.array([[1, 2], [-1, 0], [2, -3]], dtype=np.float64)
+    pl = rq.Plan(2, 3, 3, 2, [0, 1, 2], z=[3, 1, 1])
+    Y = pl.xa(dev(A)).cpu().numpy()
+    exp = np.array([[0, 0], [9 / 8, -3 / 4], [1 / 4, 3 / 2], [3 / 8, -5 / 4], [1 / 2, 1], [13 / 8, 1 / 4],
+                    [-1 / 4, 1 / 2], [7 / 8, -1 / 4]])
+    assert np.array_equal(Y, exp)
+
+
+# ------------------------------------------------------------------ general: tolerance sweep
+
+def _sweep_cases():
+    cases = []
+    rng = np.random.default_rng(2024)
+    for i in range(40):
+        b = int(rng.choice([2, 2, 3, 5]))
+        mmax = {2: 11, 3: 7, 5: 4}[b]
+        m = int(rng.integers(1, mmax + 1))
+        s = int(rng.integers(1, 65))
+        tau = int(rng.integers(1, 140))
+        kind = W.KIND_NET if (b == 2 and rng.random() < 0.3) else W.KIND_LATTICE
+        shifted = bool(rng.random() < 0.6)
+        mapping = W.MAP_INVNORM if rng.random() < 0.5 else W.MAP_UNIT
+        wmode = ["log", "rand", "zero"][int(rng.integers(0, 3))]
+        f = int(rng.integers(0, 4))
+        cases.append((1000 + i, b, m, s, tau, kind, shifted, mapping, wmode, f))
+    return cases
+
+
+@pytest.mark.parametrize("seed,b,m,s,tau,kind,shifted,mapping,wmode,f", _sweep_cases())
+def test_xa_qn_sweep(rq, seed, b, m, s, tau, kind, shifted, mapping, wmode, f):
+    """SPEC S:673-674 property sweep (b in {2,3,5}, m small, s <= 64, ragged tau, w > m, shifts)."""
+    prob = W.make_random(seed, b, m, s, tau, kind=kind, shifted=shifted, mapping=mapping, wmode=wmode, f=f)
+    p, Y, fs = run_xa(rq, prob)
+    check_y(prob, Y, np.arange(prob.N))
+    fo = oracle.f_rows(prob, np.arange(prob.N))
+    q = oracle.neumaier(fo)
+    assert abs(fs - q) <= 1e-12 * max(1e-300, np.abs(fo).sum()), (fs, q)
+    # qn (no Y) equals the fused f of xa
+    fs2 = float(p.qn_sum(dev(prob.A), prob.f, prob.fparam).item())
+    assert abs(fs2 - fs) <= 1e-13 * max(1e-300, abs(fs))
+
+
+def test_unaligned_lda_path(rq):
+    """Odd lda / odd tau (8-byte cp.async path) and a column-sliced A view."""
+    prob = W.make_random(55, 2, 10, 40, 67, shifted=True, mapping=W.MAP_INVNORM)
+    big = np.zeros((40, 71))
+    big[:, 1:68] = prob.A
+    Abig = dev(big)
+    Aview = Abig[:, 1:68]
+    pl = rq.Plan.from_problem(prob)
+    Y, fs = pl.xa(Aview, W.F_EXP_MEAN)
+    check_y(prob, Y.cpu().numpy(), np.arange(prob.N))
+
+
+# ------------------------------------------------------------------ multi-rank (simulated on one GPU)
+
+@pytest.mark.parametrize("b,m,G", [(2, 12, 2), (2, 12, 4), (2, 12, 8), (3, 7, 3), (3, 7, 9)])
+def test_simulated_ranks(rq, b, m, G):
+    """Run plan(rank=g, world=G) for every g on one GPU: local rows are k = g + G i and the sum of
+    the partial f-sums equals the world = 1 result (SURVEY §4 multi-GPU (ii))."""
+    prob = W.make_random(300 + G, b, m, 50, 40, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    A = dev(prob.A)
+    full_p = rq.Plan.from_problem(prob)
+    Yf, sf = full_p.xa(A, prob.f, prob.fparam)
+    Yf = Yf.cpu().numpy()
+    tot = 0.0
+    for g in range(G):
+        pg = rq.Plan.from_problem(prob, rank=g, world=G)
+        Yg, sg = pg.xa(A, prob.f, prob.fparam)
+        ks = g + G * np.arange(prob.N // G)
+        np.testing.assert_allclose(Yg.cpu().numpy(), Yf[ks], rtol=0, atol=1e-13 * np.abs(Yf).max())
+        tot += float(sg.item())
+    assert abs(tot - float(sf.item())) <= 1e-12 * abs(float(sf.item()))
+
+
+# ------------------------------------------------------------------ end-to-end host entry
+
+def test_qn_host_matches_device(rq):
+    prob = W.make_config("C2")
+    pl = rq.Plan.from_problem(prob)
+    d = float(pl.qn_sum(dev(prob.A), prob.f, prob.fparam).item())
+    h = pl.qn_host(prob.A, prob.f, prob.fparam)
+    assert h == d
+
+
+# ------------------------------------------------------------------ BASELINE configs
+
+def test_config_c1(rq):
+    prob = W.make_config("C1")
+    p, Y, fs = run_xa(rq, prob)
+    check_y(prob, Y, np.arange(prob.N))
+    q = oracle.qn_sum(prob)
+    assert abs(fs - q) <= 1e-12 * abs(q)
+
+
+def test_config_c2(rq):
+    prob = W.make_config("C2")
+    pl = rq.Plan.from_problem(prob)
+    fs = float(pl.qn_sum(dev(prob.A), prob.f, prob.fparam).item())
+    q = oracle.qn_sum(prob)                      # full naive oracle, 4.3e9 MACs
+    assert abs(fs - q) <= 1e-12 * abs(q)
+
+
+def _sample_rows(N, n_rand, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    ks = np.concatenate([np.arange(min(256, N)), np.arange(max(0, N - 256), N), rng.integers(0, N, n_rand),
+                         np.asarray(extra, dtype=np.int64)])
+    return np.unique(ks)
+
+
+def test_config_c3(rq):
+    prob = W.make_config("C3")
+    pl = rq.Plan.from_problem(prob)
+    A = dev(prob.A)
+    Y, fs = pl.xa(A, prob.f, prob.fparam)
+    ks = _sample_rows(prob.N, 1500, 3)
+    check_y(prob, Y[torch.from_numpy(ks).cuda()].cpu().numpy(), ks)
+    fq = float(pl.qn_sum(A, prob.f, prob.fparam).item())
+    assert fq == float(fs.item())
+    del Y
+    q = oracle.neumaier(oracle.f_all_meanid_tab(prob))   # O3' over all 2^20 rows
+    assert abs(fq - q) <= 1e-12 * abs(q)
+
+
+def test_config_c4(rq):
+    prob = W.make_config("C4")
+    pl = rq.Plan.from_problem(prob)
+    A = dev(prob.A)
+    Y, fs = pl.xa(A, prob.f, prob.fparam)            # Y stored: 17.4 GB
+    ks = _sample_rows(prob.N, 300, 4)
+    Ys = Y[torch.from_numpy(ks).cuda()].cpu().numpy()
+    check_y(prob, Ys, ks)
+    fo = oracle.f_rows(prob, ks)
+    np.testing.assert_allclose(oracle.f_of_y(Ys, prob.f, prob.fparam), fo, rtol=1e-12)
+    # the fused f equals f applied to the stored Y (fp64 on the device, fixed order)
+    fy = (Y * Y).mean(dim=1).sum().item()
+    assert abs(float(fs.item()) - fy) <= 1e-12 * abs(fy)
+    del Y
+
+
+def test_config_c5_qn_full(rq):
+    """C5 at full size in the bench's launch configuration: Q_N over all 2^24 points against the
+    oracle's O3' (g = id) computed on every row."""
+    prob = W.make_config("C5")
+    pl = rq.Plan.from_problem(prob)
+    fs = float(pl.qn_sum(dev(prob.A), prob.f, prob.fparam).item())
+    q = oracle.neumaier(oracle.f_all_meanid_tab(prob))
+    assert abs(fs - q) <= 1e-12 * abs(q), (fs, q)
+
+
+def test_config_c5_panel_rows(rq):
+    """C5 points/levels with a 64-column panel of A stored (8.6 GB), sampled rows vs the oracle."""
+    prob = W.make_config("C5")
+    prob.A = np.ascontiguousarray(prob.A[:, 1000:1064])
+    prob.tau = 64
+    pl = rq.Plan.from_problem(prob)
+    Y = pl.xa(dev(prob.A))
+    ks = _sample_rows(prob.N, 600, 5)
+    check_y(prob, Y[torch.from_numpy(ks).cuda()].cpu().numpy(), ks)

@@ -1,0 +1,167 @@
+"""Host-side checks of the C-ABI library (no GPU): exports, validation, level planner, counter law,
+residue-class partition.  SURVEY §4 test tiers 1 and 5 (partition arithmetic)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+from paper_2305_11645_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def rq():
+    _build.build()
+    import paper_2305_11645_b200 as rq
+    return rq
+
+
+def test_library_exports_every_declared_symbol(rq):
+    hdr = open(os.path.join(ROOT, "include", "rqmc.h")).read()
+    declared = set(re.findall(r"\b(rqmc_[a-z_]+)\s*\(", hdr))
+    assert declared == set(rq.EXPORTS)
+    L = C.CDLL(_build.LIB)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def _plan(rq, **kw):
+    base = dict(b=2, m=4, s=4, tau=3, w=[0, 1, 1, 2], z=[1, 1, 3, 1])
+    base.update(kw)
+    return rq.Plan(**base)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(b=4), "ENOTPRIME"),
+    (dict(w=[1, 1, 1, 2]), "EWORDER"),                         # w_1 != 0
+    (dict(w=[0, 2, 1, 2]), "EWORDER"),                         # decreasing
+    (dict(z=[2, 1, 3, 1]), "EZUNIT"),                          # even z'_1
+    (dict(z=[1, 9, 3, 1]), "EZUNIT"),                          # z'_2 >= b^{m-w_2}
+    (dict(shift=[0.0, 1.0, 0.5, 0.5]), "ESHIFT"),
+    (dict(m=40), "EUNSUPPORTED"),
+    (dict(world=3), "EUNSUPPORTED"),
+    (dict(s=0, w=[], z=[]), "EDIM"),
+])
+def test_validation_codes(rq, kw, code):
+    with pytest.raises(rq.RqmcError) as ei:
+        _plan(rq, **kw)
+    assert ei.value.name == code
+
+
+def test_net_validation(rq):
+    m = 4
+    ident = [1 << (m - 1 - q) for q in range(m)]
+    # coordinate 2 with w=1 may not depend on digit 3 (column deletion)
+    full = [8, 12, 14, 15]
+    with pytest.raises(rq.RqmcError) as ei:
+        rq.Plan(2, m, 2, 2, [0, 1], kind=rq.DIGITAL_NET, C_words=ident + full)
+    assert ei.value.name == "ENETMAT"
+    # row zeroing removes low bits first: full[3] = 15 -> row-zeroed 14, still non-zero
+    ok = [8, 12, 14, 0]
+    rq.Plan(2, m, 2, 2, [0, 1], kind=rq.DIGITAL_NET, C_words=ident + ok)
+    with pytest.raises(rq.RqmcError) as ei:
+        rq.Plan(2, m, 2, 2, [0, 1], kind=rq.DIGITAL_NET, C_words=ident + [16, 0, 0, 0])
+    assert ei.value.name == "ENETMAT"
+
+
+def test_level_table_tau_I(rq):
+    """w = (0,0,1,2,2), m = 3 -> tau_0=2, tau_1=1, tau_2=2."""
+    p = rq.Plan(2, 3, 5, 4, [0, 0, 1, 2, 2], z=[1, 3, 1, 1, 1])
+    lv = p.levels()
+    assert [(L["w"], L["s_w"], L["j_lo"], L["M"]) for L in lv] == [(2, 2, 3, 2), (1, 1, 2, 4), (0, 2, 0, 8)]
+    assert [L["parent"] for L in lv] == [-1, 0, 1]
+    assert p.summary()["s_star"] == 5
+
+
+def test_zero_columns_and_shift_level(rq):
+    """Columns j > s* are zero and dropped; with a shift they are the constant row
+    phi_j(Delta_j), kept as a 1-row level m (reading C-4)."""
+    w = [0, 1, 3, 5, 9]
+    p = rq.Plan(2, 3, 5, 2, w, z=[1, 1, 1, 1, 1])
+    assert [L["w"] for L in p.levels()] == [1, 0]
+    assert p.summary()["s_star"] == 2
+    ps = rq.Plan(2, 3, 5, 2, w, z=[1, 1, 1, 1, 1], shift=[0.1] * 5)
+    assert [(L["w"], L["s_w"], L["M"]) for L in ps.levels()] == [(3, 3, 1), (1, 1, 4), (0, 1, 8)]
+    # unshifted but mapped: Phi^-1 of the zero column is the zero-rule constant, not 0
+    pm = rq.Plan(2, 3, 5, 2, w, z=[1, 1, 1, 1, 1], map=rq.MAP_INVNORM)
+    assert [(L["w"], L["s_w"], L["M"]) for L in pm.levels()] == [(3, 3, 1), (1, 1, 4), (0, 1, 8)]
+
+
+def test_counter_law(rq):
+    """MACs = tau * sum_{j<=s*} b^{m-w_j} (SPEC S:223 counter law)."""
+    for cfg in ("C1", "C2", "C3", "C4"):
+        prob = W.make_config(cfg)
+        p = rq.Plan.from_problem(prob)
+        exp = prob.tau * sum(prob.b ** (prob.m - min(int(wj), prob.m)) for wj in prob.w if wj < prob.m)
+        assert p.stats()["macs"] == exp
+    p = rq.Plan(2, 24, 4096, 2048, W.w_log(2, 24, 4096), z=np.ones(4096, np.uint64))
+    assert p.stats()["macs"] == 2048 * (12 * 2 ** 24 + 4096)       # 4.12e11
+    assert p.levels()[p.summary()["checkpoint"]]["w"] == 6          # fused levels 0..5
+    assert p.summary()["n_fine"] == 6 and p.summary()["n_bundles"] == 2 ** 18 // 32
+
+
+def test_all_w_zero_is_dense(rq):
+    """All w_j = 0: one level, the dense product."""
+    p = rq.Plan(2, 6, 5, 3, [0] * 5, z=[1, 3, 5, 7, 9])
+    assert len(p.levels()) == 1 and p.stats()["macs"] == 64 * 5 * 3
+
+
+@pytest.mark.parametrize("b,m,G", [(2, 8, 2), (2, 8, 4), (2, 8, 8), (3, 5, 3), (3, 5, 9)])
+def test_residue_partition_covers_once(rq, b, m, G):
+    """Rank g owns k = g (mod G); the union over ranks covers 0..N-1 exactly once."""
+    s = 2 * m
+    w = W.w_log(b, m, s)
+    z = W.draw_z(3, b, m, w)
+    seen = np.zeros(b ** m, dtype=np.int64)
+    for g in range(G):
+        p = rq.Plan(b, m, s, 4, w, z=z, rank=g, world=G)
+        nl = p.summary()["N_local"]
+        assert nl == b ** m // G
+        ks = np.array([p.global_row(i) for i in range(nl)])
+        assert np.all(ks % G == g)
+        seen[ks] += 1
+        for L in p.levels():
+            assert L["M_local"] == max(L["M"] // G, 1)
+    assert np.all(seen == 1)
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    import paper_2305_11645_b200 as rq
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    prob = W.make_random(77, 2, 9, 40, 6, shifted=True, mapping=W.MAP_INVNORM)
+    p = rq.Plan.from_problem(prob, rank=rank, world=world)
+    ks = [p.global_row(i) for i in range(p.summary()["N_local"])]
+    part = torch.tensor([oracle.neumaier(oracle.f_rows(prob, ks))], dtype=torch.float64)
+    dist.all_reduce(part)                     # the path's one collective
+    q.put((rank, float(part.item()) / prob.N))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_partition_allreduce(rq):
+    """world_size-2 gloo run of the N>1 host path: each rank sums f over its residue class (via the
+    oracle on CPU), one all_reduce combines them; equals the world=1 Q_N."""
+    import multiprocessing as mp
+    import socket
+    import oracle
+    sck = socket.socket()
+    sck.bind(("127.0.0.1", 0))
+    port = sck.getsockname()[1]
+    sck.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    prob = W.make_random(77, 2, 9, 40, 6, shifted=True, mapping=W.MAP_INVNORM)
+    full = oracle.qn_sum(prob) / prob.N
+    assert abs(res[0] - full) <= 1e-13 * abs(full) and res[0] == res[1]

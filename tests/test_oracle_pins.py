@@ -371,3 +371,14 @@ def test_configs_valid():
             for j in range(p.s):
                 M = p.b ** (p.m - min(int(p.w[j]), p.m))
                 assert 1 <= int(p.z[j]) < max(M, 2) and math.gcd(int(p.z[j]), p.b) == 1
+
+
+def test_meanid_tabulated_equals_rowwise():
+    """The tabulated O3' (column periodicity) equals the row-wise O3' and the naive O3."""
+    for prob in (W.make_random(31, 2, 9, 70, 8, shifted=True, mapping=W.MAP_INVNORM),
+                 W.make_random(32, 3, 5, 30, 5, shifted=True, mapping=W.MAP_INVNORM),
+                 W.make_random(33, 2, 8, 20, 6, kind=W.KIND_NET, shifted=True)):
+        ks = np.arange(prob.N)
+        tab = oracle.f_all_meanid_tab(prob)
+        assert np.array_equal(tab, oracle.f_rows_meanid(prob, ks))
+        np.testing.assert_allclose(tab, oracle.f_rows(prob, ks), rtol=1e-13)
