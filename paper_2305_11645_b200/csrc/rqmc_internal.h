@@ -11,7 +11,8 @@ namespace rqmc {
 constexpr int kMaxLevels = 64;
 constexpr int kMaxFine = 8;       // fused fine levels (compile-time DFS depth)
 constexpr int kBundle = 32;       // residues of the checkpoint level per fine CTA
-constexpr int kFineBN = 64;       // column tile of the fine kernel
+constexpr int kFineBN = 32;       // column tile of the fine kernel
+constexpr int kFinePad = 36;      // padded t / c stride (doubles) of the fine kernel's smem tiles
 constexpr int kFineThreads = 256;
 
 // Point-generation view of one level (local rows r'' of this rank).

@@ -243,87 +243,133 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
-// a3+a4+a5: fused fine levels.  Thread (wr, wc, rp, cg): rows t0, t0+1 of the bundle and
-// columns {ca, ca+1, cb, cb+1} of the 64-wide column tile (8 doubles per path tile).
+// a3+a4+a5: fused fine levels.  CTA = bundle of kBundle (32) residues of the checkpoint level x a
+// kFineBN (32)-column tile, 8 warps in two groups; group h walks the subtrees under the top fine
+// level's runs q = h (mod 2), so the two groups never touch the same leaf row.  Inside a group the
+// 4 warps tile the 32 x 32 block as 2 x 2 warp tiles of 16 x 16 = 2 x 2 DMMA.8x8x4 fragments;
+// a path tile is 8 doubles per lane, so the whole DFS stack (one tile per fine level) lives in
+// registers.  K >= 4 steps run on the fp64 tensor pipe (mma.sync f64), K mod 4 remainders (and the
+// K = 1, 2 finest levels) as DFMA on the same accumulator registers -- no zero padding.
+// Shared memory: [A slab buf 0][A slab buf 1][X^red subtree][rowacc], t / c strides padded to 36
+// doubles so fragment loads are bank-conflict free.
 // ------------------------------------------------------------------------------------------
+constexpr int kPad = kFinePad;
+
 struct FineCtx {
-  int t0, ca, cb, wc, cg, beff;
+  int grp, wm, wn, g, tg, beff, c0;
   int64_t r0;
-  int c0;
   double* smem;
+  const double* as;      // A slab of the current column tile
 };
 
 __device__ __forceinline__ double g_of(int fk, double y, double p0) {
-  switch (fk) {
-    case 1: return exp(p0 * y);
-    case 2: return y * y;
-    default: return y;
+  return fk == 1 ? exp(p0 * y) : (fk == 2 ? y * y : y);
+}
+
+// Leaf (level 0 rows of run j): store Y and / or accumulate g into rowacc[wn][j][t].
+__device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
+  if (a.Y) {
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf) {
+      const int t = c.wm * 16 + rf * 8 + c.g;
+      if (t >= c.beff) continue;
+      double* yr = a.Y + (c.r0 + t + (int64_t)j * a.Mroot) * a.ldy;
+#pragma unroll
+      for (int cf = 0; cf < 2; ++cf) {
+        const int col = c.c0 + c.wn * 16 + cf * 8 + 2 * c.tg;
+        const double v0 = S[rf * 4 + cf * 2], v1 = S[rf * 4 + cf * 2 + 1];
+        if (col + 1 < a.tau) {
+          if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(v0, v1);
+          else { yr[col] = v0; yr[col + 1] = v1; }
+        } else if (col < a.tau) {
+          yr[col] = v0;
+        }
+      }
+    }
+  }
+  if (a.fk >= 0) {
+    double s[2];
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf) {
+      double acc = 0.0;
+#pragma unroll
+      for (int cf = 0; cf < 2; ++cf) {
+        const int col = c.c0 + c.wn * 16 + cf * 8 + 2 * c.tg;
+        if (col < a.tau) acc += g_of(a.fk, S[rf * 4 + cf * 2], a.fp0);
+        if (col + 1 < a.tau) acc += g_of(a.fk, S[rf * 4 + cf * 2 + 1], a.fp0);
+      }
+      s[rf] = acc;
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
+      s[1] += __shfl_xor_sync(0xffffffffu, s[1], o);
+    }
+    if (c.tg == 0) {
+      double* acc = c.smem + a.acc_off + ((size_t)c.wn * a.leafruns + j) * kBundle + c.wm * 16 + c.g;
+      acc[0] += s[0];
+      acc[8] += s[1];
+    }
   }
 }
 
-__device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
-  const bool v0 = c.t0 < c.beff, v1 = c.t0 + 1 < c.beff;
-  const int ga = c.c0 + c.ca, gb = c.c0 + c.cb;
-  if (a.Y) {
-    const int64_t k0 = c.r0 + c.t0 + (int64_t)j * a.Mroot;
-    double* y0 = a.Y + k0 * a.ldy;
-    double* y1 = y0 + a.ldy;
-#define RQMC_ST(ptr, col, x0, x1)                                              \
-  if ((col) + 1 < a.tau) {                                                     \
-    if (a.y_vec) *reinterpret_cast<double2*>((ptr) + (col)) = make_double2(x0, x1); \
-    else { (ptr)[col] = x0; (ptr)[(col) + 1] = x1; }                            \
-  } else if ((col) < a.tau) (ptr)[col] = x0;
-    if (v0) { RQMC_ST(y0, ga, S[0], S[1]); RQMC_ST(y0, gb, S[2], S[3]); }
-    if (v1) { RQMC_ST(y1, ga, S[4], S[5]); RQMC_ST(y1, gb, S[6], S[7]); }
-#undef RQMC_ST
+// S += X^red_w[run j] A_w for one fine level (paper Alg. 2 "+ X_I A_I").
+__device__ __forceinline__ void fine_product(const FineLevel& L, int j, const FineCtx& c, double (&S)[8]) {
+  const double* xs = c.smem + L.xs_off + (size_t)j * L.K * kPad + c.wm * 16 + c.g;
+  const double* as = c.as + L.as_off + c.wn * 16;
+  int kk = 0;
+#pragma unroll 2
+  for (; kk + 4 <= L.K; kk += 4) {
+    const double* xq = xs + (kk + c.tg) * kPad;
+    const double* aq = as + (kk + c.tg) * kPad + c.g;
+    const double a0 = xq[0], a1 = xq[8];
+    const double b0 = aq[0], b1 = aq[8];
+    double d[2];
+#define RQMC_MMA(IDX, AF, BF) d[0] = S[IDX]; d[1] = S[IDX + 1]; dmma(d, AF, BF); S[IDX] = d[0]; S[IDX + 1] = d[1];
+    RQMC_MMA(0, a0, b0)
+    RQMC_MMA(2, a0, b1)
+    RQMC_MMA(4, a1, b0)
+    RQMC_MMA(6, a1, b1)
+#undef RQMC_MMA
   }
-  if (a.fk >= 0) {
-    double s0 = 0.0, s1 = 0.0;
-    const bool ca0 = ga < a.tau, ca1 = ga + 1 < a.tau, cb0 = gb < a.tau, cb1 = gb + 1 < a.tau;
-    if (ca0) { s0 += g_of(a.fk, S[0], a.fp0); s1 += g_of(a.fk, S[4], a.fp0); }
-    if (ca1) { s0 += g_of(a.fk, S[1], a.fp0); s1 += g_of(a.fk, S[5], a.fp0); }
-    if (cb0) { s0 += g_of(a.fk, S[2], a.fp0); s1 += g_of(a.fk, S[6], a.fp0); }
-    if (cb1) { s0 += g_of(a.fk, S[3], a.fp0); s1 += g_of(a.fk, S[7], a.fp0); }
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if (c.cg == 0) {
-      double* acc = c.smem + a.acc_off + ((size_t)c.wc * a.leafruns + j) * kBundle + c.t0;
-      acc[0] += s0;
-      acc[1] += s1;
-    }
+  for (; kk < L.K; ++kk) {  // K mod 4 remainder on the DFMA pipe, same fragment layout
+    const double x0 = xs[kk * kPad], x1 = xs[kk * kPad + 8];
+    const double2 p0 = *reinterpret_cast<const double2*>(as + kk * kPad + 2 * c.tg);
+    const double2 p1 = *reinterpret_cast<const double2*>(as + kk * kPad + 8 + 2 * c.tg);
+    S[0] = fma(x0, p0.x, S[0]); S[1] = fma(x0, p0.y, S[1]);
+    S[2] = fma(x0, p1.x, S[2]); S[3] = fma(x0, p1.y, S[3]);
+    S[4] = fma(x1, p0.x, S[4]); S[5] = fma(x1, p0.y, S[5]);
+    S[6] = fma(x1, p1.x, S[6]); S[7] = fma(x1, p1.y, S[7]);
   }
 }
 
 template <int I, int NF>
-__device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
-                                           const double* as_base) {
+__device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c) {
   if constexpr (I >= NF) {
     fine_consume(a, Sp, jp, c);
   } else {
     const FineLevel& L = a.lv[I];
     const int runs_parent = (I == 0) ? 1 : a.lv[I > 0 ? I - 1 : 0].runs;
-    const double* asl = as_base + L.as_off;
-    for (int qf = 0; qf < L.fan; ++qf) {
+    const int q0 = (I == 0) ? c.grp : 0, qs = (I == 0) ? 2 : 1;  // top level split over the 2 groups
+    for (int qf = q0; qf < L.fan; qf += qs) {
       const int j = jp + qf * runs_parent;
       double S[8];
+      if (I == NF - 1 && L.K == 1) {  // finest level, K = 1: leaf = parent + x a (no copy)
+        const double* xs = c.smem + L.xs_off + (size_t)j * kPad + c.wm * 16 + c.g;
+        const double* as = c.as + L.as_off + c.wn * 16 + 2 * c.tg;
+        const double x0 = xs[0], x1 = xs[8];
+        const double2 p0 = *reinterpret_cast<const double2*>(as);
+        const double2 p1 = *reinterpret_cast<const double2*>(as + 8);
+        S[0] = fma(x0, p0.x, Sp[0]); S[1] = fma(x0, p0.y, Sp[1]);
+        S[2] = fma(x0, p1.x, Sp[2]); S[3] = fma(x0, p1.y, Sp[3]);
+        S[4] = fma(x1, p0.x, Sp[4]); S[5] = fma(x1, p0.y, Sp[5]);
+        S[6] = fma(x1, p1.x, Sp[6]); S[7] = fma(x1, p1.y, Sp[7]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) S[e] = Sp[e];
-      const double* xs = c.smem + L.xs_off + (size_t)j * L.K * kBundle + c.t0;
-      // S += X^red_w[run j] A_w  (paper Alg. 2 "+ X_I A_I")
-#pragma unroll 2
-      for (int q = 0; q < L.K; ++q) {
-        const double2 x = *reinterpret_cast<const double2*>(xs + q * kBundle);
-        const double2 pa = *reinterpret_cast<const double2*>(asl + q * kFineBN + c.ca);
-        const double2 pb = *reinterpret_cast<const double2*>(asl + q * kFineBN + c.cb);
-        S[0] = fma(x.x, pa.x, S[0]); S[1] = fma(x.x, pa.y, S[1]);
-        S[2] = fma(x.x, pb.x, S[2]); S[3] = fma(x.x, pb.y, S[3]);
-        S[4] = fma(x.y, pa.x, S[4]); S[5] = fma(x.y, pa.y, S[5]);
-        S[6] = fma(x.y, pb.x, S[6]); S[7] = fma(x.y, pb.y, S[7]);
+        for (int e = 0; e < 8; ++e) S[e] = Sp[e];
+        fine_product(L, j, c, S);
       }
-      fine_level<I + 1, NF>(a, S, j, c, as_base);
+      fine_level<I + 1, NF>(a, S, j, c);
     }
   }
 }
@@ -334,15 +380,16 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   FineCtx c;
   c.smem = smem;
-  c.wc = warp & 1;
-  c.cg = lane & 7;
-  c.t0 = (warp >> 1) * 8 + (lane >> 3) * 2;
-  c.ca = c.wc * 32 + c.cg * 2;
-  c.cb = c.ca + 16;
+  c.grp = warp >> 2;
+  c.wm = (warp >> 1) & 1;
+  c.wn = warp & 1;
+  c.g = lane >> 2;
+  c.tg = lane & 3;
   c.r0 = (int64_t)blockIdx.x * kBundle;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
 
-  // X^red of the subtree -> smem, layout [run][q][t] (t fastest); rows r0 + t + j Mroot
+  // X^red of the subtree -> smem [run][q][t] (t stride kPad); global rows r0 + t + j Mroot, read
+  // row-contiguously (t-major), written transposed.
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
     double* xs = smem + L.xs_off;
@@ -351,13 +398,13 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
       const int j = e / per_run, rem = e - j * per_run, t = rem / L.K, q = rem - t * L.K;
       double v = 0.0;
       if (t < c.beff) v = L.X[(c.r0 + t + (int64_t)j * a.Mroot) * L.ldx + q];
-      xs[((size_t)j * L.K + q) * kBundle + t] = v;
+      xs[((size_t)j * L.K + q) * kPad + t] = v;
     }
   }
   if (a.fk >= 0)
     for (int e = tid; e < 2 * a.leafruns * kBundle; e += kFineThreads) smem[a.acc_off + e] = 0.0;
 
-  // A slab of all fine levels for one column tile (double-buffered, cp.async)
+  // A slab of all fine levels for one column tile: [q][c] (c stride kPad), cp.async double buffer
   auto load_a = [&](int buf, int c0) {
     double* as = smem + buf * a.as_stride;
     for (int i = 0; i < NF; ++i) {
@@ -367,14 +414,14 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
           const int q = e / (kFineBN / 2), cc = (e % (kFineBN / 2)) * 2;
           const bool ok = c0 + cc < a.tau;
           const double* src = ok ? a.A + (int64_t)(L.j_lo + q) * a.lda + c0 + cc : a.A;
-          cp_async16(as + L.as_off + q * kFineBN + cc, src, ok);
+          cp_async16(as + L.as_off + q * kPad + cc, src, ok);
         }
       } else {
         for (int e = tid; e < L.K * kFineBN; e += kFineThreads) {
           const int q = e / kFineBN, cc = e % kFineBN;
           const bool ok = c0 + cc < a.tau;
           const double* src = ok ? a.A + (int64_t)(L.j_lo + q) * a.lda + c0 + cc : a.A;
-          cp_async8(as + L.as_off + q * kFineBN + cc, src, ok);
+          cp_async8(as + L.as_off + q * kPad + cc, src, ok);
         }
       }
     }
@@ -387,14 +434,16 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     for (int e = 0; e < 8; ++e) R[e] = 0.0;
     if (!a.root) return;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int t = c.t0 + rr;
+    for (int rf = 0; rf < 2; ++rf) {
+      const int t = c.wm * 16 + rf * 8 + c.g;
       if (t >= c.beff) continue;
       const double* p = a.root + (c.r0 + t) * a.ldroot + c0;
-      const int cols[4] = {c.ca, c.ca + 1, c.cb, c.cb + 1};
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c0 + cols[u] < a.tau) R[rr * 4 + u] = p[cols[u]];
+      for (int cf = 0; cf < 2; ++cf) {
+        const int col = c.wn * 16 + cf * 8 + 2 * c.tg;
+        if (c0 + col < a.tau) R[rf * 4 + cf * 2] = p[col];
+        if (c0 + col + 1 < a.tau) R[rf * 4 + cf * 2 + 1] = p[col + 1];
+      }
     }
   };
 
@@ -403,6 +452,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   load_root(Rnext, 0);
   for (int ct = 0; ct < ntiles; ++ct) {
     c.c0 = ct * kFineBN;
+    c.as = smem + (ct & 1) * a.as_stride;
     double Sroot[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) Sroot[e] = Rnext[e];
@@ -416,7 +466,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     }
     __syncthreads();  // A slab of this tile (and X, rowacc on the first pass) visible
     if (ct + 1 < ntiles) load_root(Rnext, (ct + 1) * kFineBN);
-    fine_level<0, NF>(a, Sroot, 0, c, smem + (ct & 1) * a.as_stride);
+    if (NF > 0 || c.grp == 0) fine_level<0, NF>(a, Sroot, 0, c);
     __syncthreads();  // buffer (ct & 1) is refilled at iteration ct + 1
   }
 

@@ -102,8 +102,8 @@ int fine_smem_bytes(const rqmc_plan_s& p, int c, std::vector<int>* xs_off, std::
     const int64_t runs = p.lv[i].Ml / Mroot;
     if (xs_off) xs_off->push_back((int)xs);
     if (as_off) as_off->push_back((int)as);
-    xs += (size_t)runs * p.lv[i].s_w * kBundle;
-    as += (size_t)p.lv[i].s_w * kFineBN;
+    xs += (size_t)runs * p.lv[i].s_w * kFinePad;
+    as += (size_t)p.lv[i].s_w * kFinePad;
     lr = (int)runs;
   }
   xs = align_up(xs, 2);
