@@ -58,6 +58,7 @@ struct FineArgs {
   double* partial;
   int leafruns;
   int as_stride;      // doubles per A buffer
+  int root_off;       // root tile buffers offset (doubles), 2 x kBundle x kFinePad
   int acc_off;        // rowacc offset (doubles)
   int smem_bytes;
 };

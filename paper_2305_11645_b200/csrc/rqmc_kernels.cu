@@ -245,107 +245,240 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // a3+a4+a5: fused fine levels.  CTA = bundle of kBundle (32) residues of the checkpoint level x a
 // kFineBN (32)-column tile, 8 warps in two groups; group h walks the subtrees under the top fine
-// level's runs q = h (mod 2), so the two groups never touch the same leaf row.  Inside a group the
-// 4 warps tile the 32 x 32 block as 2 x 2 warp tiles of 16 x 16 = 2 x 2 DMMA.8x8x4 fragments;
-// a path tile is 8 doubles per lane, so the whole DFS stack (one tile per fine level) lives in
-// registers.  K >= 4 steps run on the fp64 tensor pipe (mma.sync f64), K mod 4 remainders (and the
-// K = 1, 2 finest levels) as DFMA on the same accumulator registers -- no zero padding.
-// Shared memory: [A slab buf 0][A slab buf 1][X^red subtree][rowacc], t / c strides padded to 36
-// doubles so fragment loads are bank-conflict free.
+// level's runs q = h (mod 2), so the two groups never touch the same leaf row.  In a group, warp
+// wm owns rows 8 wm .. 8 wm + 7 of every run and all 32 columns = 1 x 4 DMMA.8x8x4 fragments, so a
+// path tile is 8 doubles per lane and one lane's 8 leaf values share ONE row (cheap row sums).
+// The DFS stack (one tile per fine level) lives in registers.  K >= 4 steps run on the fp64 tensor
+// pipe (mma.sync f64 with C and D in different registers: no stack copies), K mod 4 remainders and
+// K < 4 levels as DFMA on the same fragment registers (no zero padding).
+// The bottom NB levels of common shapes (BT) are compile-time: fans and K known, loops unrolled,
+// leaf consumption (Y store, g) templated, so the per-leaf control overhead disappears.
+// Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36 doubles
+// (bank-conflict-free fragment loads).  Columns >= tau are zero in the A slab and the root tile, so
+// leaf values there are exactly 0 and need no mask (g = exp is corrected in the finalisation).
 // ------------------------------------------------------------------------------------------
 constexpr int kPad = kFinePad;
 
 struct FineCtx {
-  int grp, wm, wn, g, tg, beff, c0;
+  int grp, wm, g, tg, t, beff, c0;
   int64_t r0;
-  double* smem;
   const double* as;      // A slab of the current column tile
 };
 
-__device__ __forceinline__ double g_of(int fk, double y, double p0) {
-  return fk == 1 ? exp(p0 * y) : (fk == 2 ? y * y : y);
+// D = A B + C with C and D in distinct registers (DMMA.8x8x4)
+__device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// Leaf (level 0 rows of run j): store Y and / or accumulate g into rowacc[wn][j][t].
-__device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
-  if (a.Y) {
+extern __shared__ __align__(16) double fsm[];
+
+// ---- g kinds (f(y) = F(tau^-1 sum_c g(y_c)), reading C-17): 0 none, 1 identity, 2 exp(p0 y), 3 y^2
+template <int G>
+__device__ __forceinline__ double gsum8(const double (&S)[8], double p0) {
+  if constexpr (G == 2) {
+    double v = exp(p0 * S[0]);
 #pragma unroll
-    for (int rf = 0; rf < 2; ++rf) {
-      const int t = c.wm * 16 + rf * 8 + c.g;
-      if (t >= c.beff) continue;
-      double* yr = a.Y + (c.r0 + t + (int64_t)j * a.Mroot) * a.ldy;
+    for (int e = 1; e < 8; ++e) v += exp(p0 * S[e]);
+    return v;
+  } else if constexpr (G == 3) {
+    double v = S[0] * S[0];
 #pragma unroll
-      for (int cf = 0; cf < 2; ++cf) {
-        const int col = c.c0 + c.wn * 16 + cf * 8 + 2 * c.tg;
-        const double v0 = S[rf * 4 + cf * 2], v1 = S[rf * 4 + cf * 2 + 1];
+    for (int e = 1; e < 8; ++e) v = fma(S[e], S[e], v);
+    return v;
+  } else {
+    return ((S[0] + S[1]) + (S[2] + S[3])) + ((S[4] + S[5]) + (S[6] + S[7]));
+  }
+}
+
+template <bool STY>
+__device__ __forceinline__ void store_leaf(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
+  if constexpr (STY) {
+    if (c.t < c.beff) {
+      double* yr = a.Y + (c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) {
+        const int col = c.c0 + cf * 8 + 2 * c.tg;
         if (col + 1 < a.tau) {
-          if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(v0, v1);
-          else { yr[col] = v0; yr[col + 1] = v1; }
+          if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(S[2 * cf], S[2 * cf + 1]);
+          else { yr[col] = S[2 * cf]; yr[col + 1] = S[2 * cf + 1]; }
         } else if (col < a.tau) {
-          yr[col] = v0;
+          yr[col] = S[2 * cf];
         }
       }
     }
   }
-  if (a.fk >= 0) {
-    double s[2];
-#pragma unroll
-    for (int rf = 0; rf < 2; ++rf) {
-      double acc = 0.0;
-#pragma unroll
-      for (int cf = 0; cf < 2; ++cf) {
-        const int col = c.c0 + c.wn * 16 + cf * 8 + 2 * c.tg;
-        if (col < a.tau) acc += g_of(a.fk, S[rf * 4 + cf * 2], a.fp0);
-        if (col + 1 < a.tau) acc += g_of(a.fk, S[rf * 4 + cf * 2 + 1], a.fp0);
-      }
-      s[rf] = acc;
-    }
-#pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
-      s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
-      s[1] += __shfl_xor_sync(0xffffffffu, s[1], o);
-    }
-    if (c.tg == 0) {
-      double* acc = c.smem + a.acc_off + ((size_t)c.wn * a.leafruns + j) * kBundle + c.wm * 16 + c.g;
-      acc[0] += s[0];
-      acc[8] += s[1];
-    }
-  }
 }
 
-// S += X^red_w[run j] A_w for one fine level (paper Alg. 2 "+ X_I A_I").
-__device__ __forceinline__ void fine_product(const FineLevel& L, int j, const FineCtx& c, double (&S)[8]) {
-  const double* xs = c.smem + L.xs_off + (size_t)j * L.K * kPad + c.wm * 16 + c.g;
-  const double* as = c.as + L.as_off + c.wn * 16;
+// S = Sp + X^red_w[run] A_w for one level with compile-time K (<= 0: runtime L.K)
+// (paper Alg. 2 "tile(P_{I+1}) + X_I A_I").  xs: X^red of the run at this lane's row.
+template <int KC>
+__device__ __forceinline__ void level_step(const double* xs, const double* as, int Krt, const FineCtx& c,
+                                           const double (&Sp)[8], double (&S)[8]) {
+  const int K = KC > 0 ? KC : Krt;
   int kk = 0;
+  if (K >= 4) {
+    {
+      const double af = xs[c.tg * kPad];
+      const double* aq = as + c.tg * kPad + c.g;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, aq[cf * 8], Sp[2 * cf], Sp[2 * cf + 1]);
+    }
+    kk = 4;
 #pragma unroll 2
-  for (; kk + 4 <= L.K; kk += 4) {
-    const double* xq = xs + (kk + c.tg) * kPad;
-    const double* aq = as + (kk + c.tg) * kPad + c.g;
-    const double a0 = xq[0], a1 = xq[8];
-    const double b0 = aq[0], b1 = aq[8];
-    double d[2];
-#define RQMC_MMA(IDX, AF, BF) d[0] = S[IDX]; d[1] = S[IDX + 1]; dmma(d, AF, BF); S[IDX] = d[0]; S[IDX + 1] = d[1];
-    RQMC_MMA(0, a0, b0)
-    RQMC_MMA(2, a0, b1)
-    RQMC_MMA(4, a1, b0)
-    RQMC_MMA(6, a1, b1)
-#undef RQMC_MMA
+    for (; kk + 4 <= K; kk += 4) {
+      const double af = xs[(kk + c.tg) * kPad];
+      const double* aq = as + (kk + c.tg) * kPad + c.g;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, aq[cf * 8], S[2 * cf], S[2 * cf + 1]);
+    }
+  } else {
+    const double x = xs[0];
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf) {
+      const double2 p = *reinterpret_cast<const double2*>(as + cf * 8 + 2 * c.tg);
+      S[2 * cf] = fma(x, p.x, Sp[2 * cf]);
+      S[2 * cf + 1] = fma(x, p.y, Sp[2 * cf + 1]);
+    }
+    kk = 1;
   }
-  for (; kk < L.K; ++kk) {  // K mod 4 remainder on the DFMA pipe, same fragment layout
-    const double x0 = xs[kk * kPad], x1 = xs[kk * kPad + 8];
-    const double2 p0 = *reinterpret_cast<const double2*>(as + kk * kPad + 2 * c.tg);
-    const double2 p1 = *reinterpret_cast<const double2*>(as + kk * kPad + 8 + 2 * c.tg);
-    S[0] = fma(x0, p0.x, S[0]); S[1] = fma(x0, p0.y, S[1]);
-    S[2] = fma(x0, p1.x, S[2]); S[3] = fma(x0, p1.y, S[3]);
-    S[4] = fma(x1, p0.x, S[4]); S[5] = fma(x1, p0.y, S[5]);
-    S[6] = fma(x1, p1.x, S[6]); S[7] = fma(x1, p1.y, S[7]);
+#pragma unroll
+  for (; kk < K; ++kk) {  // K mod 4 remainder on the DFMA pipe, same fragment layout
+    const double x = xs[kk * kPad];
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf) {
+      const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + cf * 8 + 2 * c.tg);
+      S[2 * cf] = fma(x, p.x, S[2 * cf]);
+      S[2 * cf + 1] = fma(x, p.y, S[2 * cf + 1]);
+    }
   }
 }
 
-template <int I, int NF>
-__device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c) {
-  if constexpr (I >= NF) {
+// Compile-time description of the bottom NB fine levels (index 0 = coarsest of them).
+template <int NB_, int F0, int K0, int F1, int K1, int F2, int K2>
+struct Bot {
+  static constexpr int NB = NB_;
+  __host__ __device__ static constexpr int fan(int i) { return i == 0 ? F0 : (i == 1 ? F1 : F2); }
+  __host__ __device__ static constexpr int k(int i) { return i == 0 ? K0 : (i == 1 ? K1 : K2); }
+  __host__ __device__ static constexpr int kleaf() { return k(NB_ - 1); }
+};
+using BotNone = Bot<0, 0, 0, 0, 0, 0, 0>;
+using BotB2 = Bot<3, 2, 4, 2, 2, 2, 1>;   // b = 2, w_j = floor(log2 j): K = 4, 2, 1, fans 2
+using BotB2s = Bot<2, 2, 2, 2, 1, 0, 0>;  // b = 2, only two fine levels below: K = 2, 1
+using BotB3 = Bot<2, 3, 6, 3, 2, 0, 0>;   // b = 3, w_j = floor(log3 j): K = 6, 2, fans 3
+
+template <int KL>
+struct LeafCache { double v[KL > 0 && KL <= 2 ? KL : 1][8]; };
+
+// Leaf level of the bottom block: F children of the parent tile Sp; Y store + g, batched row sums.
+template <int NF, class BT, int G, bool STY>
+__device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
+                                           const LeafCache<BT::kleaf()>& lc) {
+  constexpr int BL = BT::NB - 1, I = NF - 1, F = BT::fan(BL), K = BT::k(BL);
+  const FineLevel& L = a.lv[I];
+  const int runs_parent = (I == 0) ? 1 : a.lv[I > 0 ? I - 1 : 0].runs;
+  double v[F];
+  auto leaf = [&](int q) {
+    const int j = jp + q * runs_parent;
+    const double* xs = fsm + L.xs_off + j * K * kPad + c.t;
+    double S[8];
+    if constexpr (K <= 2) {
+      const double x0 = xs[0];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) S[e] = fma(x0, lc.v[0][e], Sp[e]);
+      if constexpr (K == 2) {
+        const double x1 = xs[kPad];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) S[e] = fma(x1, lc.v[1][e], S[e]);
+      }
+    } else {
+      level_step<K>(xs, c.as + L.as_off, K, c, Sp, S);
+    }
+    store_leaf<STY>(a, S, j, c);
+    if constexpr (G > 0) v[q] = gsum8<G>(S, a.fp0);
+  };
+  if constexpr (I == 0) {
+    for (int q = c.grp; q < F; q += 2) leaf(q);
+  } else {
+#pragma unroll
+    for (int q = 0; q < F; ++q) leaf(q);
+  }
+  if constexpr (G > 0) {
+    if constexpr (I == 0) {  // (degenerate: leaf level is the top level) one leaf at a time
+      for (int q = c.grp; q < F; q += 2) {
+        double s = v[q];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (c.tg == 0) fsm[a.acc_off + q * kBundle + c.t] += s;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < F; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 1);
+#pragma unroll
+      for (int q = 0; q < F; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
+      if (c.tg == 0) {
+#pragma unroll
+        for (int q = 0; q < F; ++q) fsm[a.acc_off + (jp + q * runs_parent) * kBundle + c.t] += v[q];
+      }
+    }
+  }
+}
+
+template <int NF, int BL, class BT, int G, bool STY>
+__device__ __forceinline__ void bot_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
+                                          const LeafCache<BT::kleaf()>& lc) {
+  if constexpr (BL == BT::NB - 1) {
+    bot_leaves<NF, BT, G, STY>(a, Sp, jp, c, lc);
+  } else {
+    constexpr int I = NF - BT::NB + BL, F = BT::fan(BL), K = BT::k(BL);
+    const FineLevel& L = a.lv[I];
+    const int runs_parent = (I == 0) ? 1 : a.lv[I > 0 ? I - 1 : 0].runs;
+    auto child = [&](int q) {
+      const int j = jp + q * runs_parent;
+      double S[8];
+      level_step<K>(fsm + L.xs_off + j * K * kPad + c.t, c.as + L.as_off, K, c, Sp, S);
+      bot_level<NF, BL + 1, BT, G, STY>(a, S, j, c, lc);
+    };
+    if constexpr (I == 0) {
+      for (int q = c.grp; q < F; q += 2) child(q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < F; ++q) child(q);
+    }
+  }
+}
+
+template <int NF, class BT>
+__device__ __forceinline__ void bot_dispatch(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
+                                             const LeafCache<BT::kleaf()>& lc) {
+  const bool sty = a.Y != nullptr;
+  switch (a.fk) {
+    case -1: sty ? bot_level<NF, 0, BT, 0, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 0, false>(a, Sp, jp, c, lc); break;
+    case 1: sty ? bot_level<NF, 0, BT, 2, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 2, false>(a, Sp, jp, c, lc); break;
+    case 2: sty ? bot_level<NF, 0, BT, 3, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 3, false>(a, Sp, jp, c, lc); break;
+    default: sty ? bot_level<NF, 0, BT, 1, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 1, false>(a, Sp, jp, c, lc); break;
+  }
+}
+
+// Generic leaf consumption (runtime g / Y), used when the bottom shape is not specialised.
+__device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
+  if (a.Y) store_leaf<true>(a, S, j, c);
+  if (a.fk >= 0) {
+    double v = a.fk == 1 ? gsum8<2>(S, a.fp0) : (a.fk == 2 ? gsum8<3>(S, a.fp0) : gsum8<1>(S, a.fp0));
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (c.tg == 0) fsm[a.acc_off + j * kBundle + c.t] += v;
+  }
+}
+
+// Upper fine levels: runtime fans / K, register stack; hands over to the bottom block.
+template <int I, int NF, class BT>
+__device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
+                                           const LeafCache<BT::kleaf()>& lc) {
+  if constexpr (BT::NB > 0 && I == NF - BT::NB) {
+    bot_dispatch<NF, BT>(a, Sp, jp, c, lc);
+  } else if constexpr (I >= NF) {
     fine_consume(a, Sp, jp, c);
   } else {
     const FineLevel& L = a.lv[I];
@@ -354,69 +487,58 @@ __device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)
     for (int qf = q0; qf < L.fan; qf += qs) {
       const int j = jp + qf * runs_parent;
       double S[8];
-      if (I == NF - 1 && L.K == 1) {  // finest level, K = 1: leaf = parent + x a (no copy)
-        const double* xs = c.smem + L.xs_off + (size_t)j * kPad + c.wm * 16 + c.g;
-        const double* as = c.as + L.as_off + c.wn * 16 + 2 * c.tg;
-        const double x0 = xs[0], x1 = xs[8];
-        const double2 p0 = *reinterpret_cast<const double2*>(as);
-        const double2 p1 = *reinterpret_cast<const double2*>(as + 8);
-        S[0] = fma(x0, p0.x, Sp[0]); S[1] = fma(x0, p0.y, Sp[1]);
-        S[2] = fma(x0, p1.x, Sp[2]); S[3] = fma(x0, p1.y, Sp[3]);
-        S[4] = fma(x1, p0.x, Sp[4]); S[5] = fma(x1, p0.y, Sp[5]);
-        S[6] = fma(x1, p1.x, Sp[6]); S[7] = fma(x1, p1.y, Sp[7]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) S[e] = Sp[e];
-        fine_product(L, j, c, S);
-      }
-      fine_level<I + 1, NF>(a, S, j, c);
+      level_step<0>(fsm + L.xs_off + j * L.K * kPad + c.t, c.as + L.as_off, L.K, c, Sp, S);
+      fine_level<I + 1, NF, BT>(a, S, j, c, lc);
     }
   }
 }
 
-template <int NF>
+template <int NF, class BT>
 __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
-  extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   FineCtx c;
-  c.smem = smem;
   c.grp = warp >> 2;
-  c.wm = (warp >> 1) & 1;
-  c.wn = warp & 1;
+  c.wm = warp & 3;
   c.g = lane >> 2;
   c.tg = lane & 3;
+  c.t = c.wm * 8 + c.g;
   c.r0 = (int64_t)blockIdx.x * kBundle;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
 
   // X^red of the subtree -> smem [run][q][t] (t stride kPad); global rows r0 + t + j Mroot, read
-  // row-contiguously (t-major), written transposed.
+  // row-contiguously, written transposed.
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
-    double* xs = smem + L.xs_off;
+    double* xs = fsm + L.xs_off;
     const int per_run = kBundle * L.K;
     for (int e = tid; e < L.runs * per_run; e += kFineThreads) {
       const int j = e / per_run, rem = e - j * per_run, t = rem / L.K, q = rem - t * L.K;
       double v = 0.0;
       if (t < c.beff) v = L.X[(c.r0 + t + (int64_t)j * a.Mroot) * L.ldx + q];
-      xs[((size_t)j * L.K + q) * kPad + t] = v;
+      xs[(j * L.K + q) * kPad + t] = v;
     }
   }
   if (a.fk >= 0)
-    for (int e = tid; e < 2 * a.leafruns * kBundle; e += kFineThreads) smem[a.acc_off + e] = 0.0;
+    for (int e = tid; e < a.leafruns * kBundle; e += kFineThreads) fsm[a.acc_off + e] = 0.0;
 
-  // A slab of all fine levels for one column tile: [q][c] (c stride kPad), cp.async double buffer
-  auto load_a = [&](int buf, int c0) {
-    double* as = smem + buf * a.as_stride;
-    for (int i = 0; i < NF; ++i) {
-      const FineLevel& L = a.lv[i];
-      if (a.a_vec) {
+  // One column tile's operands, cp.async double buffer: the A slab of all fine levels [q][c] and the
+  // root tile R_ckpt[t][c] (c stride kPad); zero-filled beyond tau / the bundle.
+  auto load_tile = [&](int buf, int c0) {
+    double* as = fsm + buf * a.as_stride;
+    double* rs = fsm + a.root_off + buf * (kBundle * kPad);
+    if (a.a_vec) {
+      for (int i = 0; i < NF; ++i) {
+        const FineLevel& L = a.lv[i];
         for (int e = tid; e < L.K * (kFineBN / 2); e += kFineThreads) {
           const int q = e / (kFineBN / 2), cc = (e % (kFineBN / 2)) * 2;
           const bool ok = c0 + cc < a.tau;
           const double* src = ok ? a.A + (int64_t)(L.j_lo + q) * a.lda + c0 + cc : a.A;
           cp_async16(as + L.as_off + q * kPad + cc, src, ok);
         }
-      } else {
+      }
+    } else {
+      for (int i = 0; i < NF; ++i) {
+        const FineLevel& L = a.lv[i];
         for (int e = tid; e < L.K * kFineBN; e += kFineThreads) {
           const int q = e / kFineBN, cc = e % kFineBN;
           const bool ok = c0 + cc < a.tau;
@@ -425,58 +547,69 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
         }
       }
     }
+    // root rows: ldroot even and c0 even -> 16B chunks; a chunk is valid iff its first column is
+    // (tau may be odd: the second element of the last chunk is then masked by a scalar copy)
+    for (int e = tid; e < kBundle * (kFineBN / 2); e += kFineThreads) {
+      const int t = e / (kFineBN / 2), cc = (e % (kFineBN / 2)) * 2;
+      const bool row_ok = a.root != nullptr && t < c.beff;
+      const double* src = a.root + (c.r0 + t) * a.ldroot + c0 + cc;
+      if (c0 + cc + 1 < a.tau || !row_ok) {
+        cp_async16(rs + t * kPad + cc, row_ok ? src : a.A, row_ok);
+      } else {  // last, odd column: copy one element, zero the other
+        cp_async8(rs + t * kPad + cc, row_ok && c0 + cc < a.tau ? src : a.A, row_ok && c0 + cc < a.tau);
+        cp_async8(rs + t * kPad + cc + 1, a.A, false);
+      }
+    }
     cp_async_commit();
   };
 
   const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
-  auto load_root = [&](double (&R)[8], int c0) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) R[e] = 0.0;
-    if (!a.root) return;
-#pragma unroll
-    for (int rf = 0; rf < 2; ++rf) {
-      const int t = c.wm * 16 + rf * 8 + c.g;
-      if (t >= c.beff) continue;
-      const double* p = a.root + (c.r0 + t) * a.ldroot + c0;
-#pragma unroll
-      for (int cf = 0; cf < 2; ++cf) {
-        const int col = c.wn * 16 + cf * 8 + 2 * c.tg;
-        if (c0 + col < a.tau) R[rf * 4 + cf * 2] = p[col];
-        if (c0 + col + 1 < a.tau) R[rf * 4 + cf * 2 + 1] = p[col + 1];
-      }
-    }
-  };
-
-  if (NF > 0) load_a(0, 0);
-  double Rnext[8];
-  load_root(Rnext, 0);
+  load_tile(0, 0);
   for (int ct = 0; ct < ntiles; ++ct) {
     c.c0 = ct * kFineBN;
-    c.as = smem + (ct & 1) * a.as_stride;
+    c.as = fsm + (ct & 1) * a.as_stride;
+    if (ct + 1 < ntiles) {
+      load_tile((ct + 1) & 1, (ct + 1) * kFineBN);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // operands of this tile (and X, rowacc on the first pass) visible
     double Sroot[8];
+    {
+      const double* rs = fsm + a.root_off + (ct & 1) * (kBundle * kPad) + c.t * kPad + 2 * c.tg;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) Sroot[e] = Rnext[e];
-    if (NF > 0) {
-      if (ct + 1 < ntiles) {
-        load_a((ct + 1) & 1, (ct + 1) * kFineBN);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+      for (int cf = 0; cf < 4; ++cf) {
+        const double2 p = *reinterpret_cast<const double2*>(rs + cf * 8);
+        Sroot[2 * cf] = p.x;
+        Sroot[2 * cf + 1] = p.y;
       }
     }
-    __syncthreads();  // A slab of this tile (and X, rowacc on the first pass) visible
-    if (ct + 1 < ntiles) load_root(Rnext, (ct + 1) * kFineBN);
-    if (NF > 0 || c.grp == 0) fine_level<0, NF>(a, Sroot, 0, c);
-    __syncthreads();  // buffer (ct & 1) is refilled at iteration ct + 1
+    LeafCache<BT::kleaf()> lc;
+    if constexpr (BT::NB > 0 && BT::kleaf() <= 2) {
+      const FineLevel& L = a.lv[NF - 1];
+#pragma unroll
+      for (int q = 0; q < BT::kleaf(); ++q)
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) {
+          const double2 p = *reinterpret_cast<const double2*>(c.as + L.as_off + q * kPad + cf * 8 + 2 * c.tg);
+          lc.v[q][2 * cf] = p.x;
+          lc.v[q][2 * cf + 1] = p.y;
+        }
+    }
+    if (NF > 0 || c.grp == 0) fine_level<0, NF, BT>(a, Sroot, 0, c, lc);
+    __syncthreads();  // buffers (ct & 1) are refilled at iteration ct + 1
   }
 
   if (a.fk >= 0) {
-    // F(tau^-1 sum_c g) per leaf row, then a fixed-order CTA reduction -> partial[bundle]
+    // F(tau^-1 sum_c g) per leaf row, then a fixed-order CTA reduction -> partial[bundle].
+    // Padded columns (>= tau) hold y = 0 exactly: g(0) = 0 except g = exp, which added exp(0) = 1.
+    const double pad = a.fk == 1 ? (double)(ntiles * kFineBN - a.tau) : 0.0;
     double part = 0.0;
     for (int e = tid; e < a.leafruns * kBundle; e += kFineThreads) {
       const int t = e % kBundle;
       if (t >= c.beff) continue;
-      const double rs = smem[a.acc_off + e] + smem[a.acc_off + a.leafruns * kBundle + e];
+      const double rs = fsm[a.acc_off + e] - pad;
       const double mean = rs / a.tau;
       double fv;
       switch (a.fk) {
@@ -499,25 +632,47 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   }
 }
 
-template <int NF>
+template <int NF, class BT>
 static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_fine<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+  cudaError_t e = cudaFuncSetAttribute(k_fine<NF, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
   if (e != cudaSuccess) return e;
-  k_fine<NF><<<(unsigned)nb, kFineThreads, a.smem_bytes, st>>>(a);
+  k_fine<NF, BT><<<(unsigned)nb, kFineThreads, a.smem_bytes, st>>>(a);
   return cudaGetLastError();
+}
+
+// Does the bottom of the fine level table match the compile-time shape BT?
+template <class BT>
+static bool bottom_matches(const FineArgs& a) {
+  if (a.NF < BT::NB) return false;
+  for (int i = 0; i < BT::NB; ++i) {
+    const FineLevel& L = a.lv[a.NF - BT::NB + i];
+    if (L.fan != BT::fan(i) || L.K != BT::k(i)) return false;
+  }
+  return true;
+}
+
+template <int NF>
+static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, cudaStream_t st) {
+  if constexpr (NF >= 3)
+    if (bottom_matches<BotB2>(a)) return launch_fine_t<NF, BotB2>(a, nb, st);
+  if constexpr (NF >= 2) {
+    if (bottom_matches<BotB2s>(a)) return launch_fine_t<NF, BotB2s>(a, nb, st);
+    if (bottom_matches<BotB3>(a)) return launch_fine_t<NF, BotB3>(a, nb, st);
+  }
+  return launch_fine_t<NF, BotNone>(a, nb, st);
 }
 
 cudaError_t launch_fine(const FineArgs& a, int64_t nb, cudaStream_t st) {
   switch (a.NF) {
-    case 0: return launch_fine_t<0>(a, nb, st);
-    case 1: return launch_fine_t<1>(a, nb, st);
-    case 2: return launch_fine_t<2>(a, nb, st);
-    case 3: return launch_fine_t<3>(a, nb, st);
-    case 4: return launch_fine_t<4>(a, nb, st);
-    case 5: return launch_fine_t<5>(a, nb, st);
-    case 6: return launch_fine_t<6>(a, nb, st);
-    case 7: return launch_fine_t<7>(a, nb, st);
-    case 8: return launch_fine_t<8>(a, nb, st);
+    case 0: return launch_fine_t<0, BotNone>(a, nb, st);
+    case 1: return launch_fine_n<1>(a, nb, st);
+    case 2: return launch_fine_n<2>(a, nb, st);
+    case 3: return launch_fine_n<3>(a, nb, st);
+    case 4: return launch_fine_n<4>(a, nb, st);
+    case 5: return launch_fine_n<5>(a, nb, st);
+    case 6: return launch_fine_n<6>(a, nb, st);
+    case 7: return launch_fine_n<7>(a, nb, st);
+    case 8: return launch_fine_n<8>(a, nb, st);
     default: return cudaErrorInvalidValue;
   }
 }

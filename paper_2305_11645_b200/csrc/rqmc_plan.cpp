@@ -108,14 +108,15 @@ int fine_smem_bytes(const rqmc_plan_s& p, int c, std::vector<int>* xs_off, std::
   }
   xs = align_up(xs, 2);
   as = align_up(as, 2);
-  const size_t acc = 2 * (size_t)lr * kBundle;
-  // layout: [A buf 0][A buf 1][X subtree][rowacc]
+  const size_t acc = (size_t)lr * kBundle;  // one row-sum slot per leaf row (groups are disjoint)
+  // layout: [A buf 0][A buf 1][root buf 0][root buf 1][X subtree][rowacc]
+  const size_t roots = 2 * (size_t)kBundle * kFinePad;
   if (as_stride) *as_stride = (int)as;
   if (xs_off)
-    for (auto& o : *xs_off) o += (int)(2 * as);
-  if (acc_off) *acc_off = (int)(2 * as + xs);
+    for (auto& o : *xs_off) o += (int)(2 * as + roots);
+  if (acc_off) *acc_off = (int)(2 * as + roots + xs);
   if (leafruns) *leafruns = lr;
-  return (int)((2 * as + xs + acc) * sizeof(double));
+  return (int)((2 * as + roots + xs + acc) * sizeof(double));
 }
 
 constexpr int kFineSmemLimit = 200 * 1024;
@@ -463,6 +464,7 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   fa.partial = reinterpret_cast<double*>(w + p->off_part);
   fa.leafruns = p->leafruns;
   fa.as_stride = p->fine_as_stride;
+  fa.root_off = 2 * p->fine_as_stride;
   fa.acc_off = p->fine_acc_off;
   fa.smem_bytes = p->fine_smem;
   if (rqmc_status s = check_cuda(p, launch_fine(fa, p->nbundles, st), "k_fine")) return s;
