@@ -368,16 +368,31 @@ using BotB2 = Bot<3, 2, 4, 2, 2, 2, 1>;   // b = 2, w_j = floor(log2 j): K = 4, 
 using BotB2s = Bot<2, 2, 2, 2, 1, 0, 0>;  // b = 2, only two fine levels below: K = 2, 1
 using BotB3 = Bot<2, 3, 6, 3, 2, 0, 0>;   // b = 3, w_j = floor(log3 j): K = 6, 2, fans 3
 
-template <int KL>
-struct LeafCache { double v[KL > 0 && KL <= 2 ? KL : 1][8]; };
+// Per-column-tile register cache of the bottom block: the leaf level's A values (K <= 2, used by
+// DFMA), the B fragments of a K = 4 bottom level (one DMMA step), and the parent run counts.
+template <class BT>
+struct LeafCache {
+  static constexpr int KL = BT::kleaf();
+  static constexpr bool CL = BT::NB > 0 && KL <= 2;
+  static constexpr bool C4 = BT::NB == 3 && BT::k(0) == 4;
+  double v[CL ? KL : 1][8];
+  double b4[4];
+  int runs[3];
+};
+
+// Non-returning shared-memory add (red.shared.add.f64): each rowacc slot is updated by exactly one
+// lane per column tile, so the accumulation order stays fixed (deterministic).
+__device__ __forceinline__ void red_add_shared(double* p, double v) {
+  asm volatile("red.shared.add.f64 [%0], %1;\n" ::"r"(smem_u32(p)), "d"(v) : "memory");
+}
 
 // Leaf level of the bottom block: F children of the parent tile Sp; Y store + g, batched row sums.
 template <int NF, class BT, int G, bool STY>
 __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
-                                           const LeafCache<BT::kleaf()>& lc) {
+                                           const LeafCache<BT>& lc) {
   constexpr int BL = BT::NB - 1, I = NF - 1, F = BT::fan(BL), K = BT::k(BL);
   const FineLevel& L = a.lv[I];
-  const int runs_parent = (I == 0) ? 1 : a.lv[I > 0 ? I - 1 : 0].runs;
+  const int runs_parent = lc.runs[BL];
   double v[F];
   auto leaf = [&](int q) {
     const int j = jp + q * runs_parent;
@@ -410,7 +425,7 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
         double s = v[q];
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (c.tg == 0) fsm[a.acc_off + q * kBundle + c.t] += s;
+        if (c.tg == 0) red_add_shared(fsm + a.acc_off + q * kBundle + c.t, s);
       }
     } else {
 #pragma unroll
@@ -419,7 +434,7 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
       for (int q = 0; q < F; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
       if (c.tg == 0) {
 #pragma unroll
-        for (int q = 0; q < F; ++q) fsm[a.acc_off + (jp + q * runs_parent) * kBundle + c.t] += v[q];
+        for (int q = 0; q < F; ++q) red_add_shared(fsm + a.acc_off + (jp + q * runs_parent) * kBundle + c.t, v[q]);
       }
     }
   }
@@ -427,17 +442,23 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
 
 template <int NF, int BL, class BT, int G, bool STY>
 __device__ __forceinline__ void bot_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
-                                          const LeafCache<BT::kleaf()>& lc) {
+                                          const LeafCache<BT>& lc) {
   if constexpr (BL == BT::NB - 1) {
     bot_leaves<NF, BT, G, STY>(a, Sp, jp, c, lc);
   } else {
     constexpr int I = NF - BT::NB + BL, F = BT::fan(BL), K = BT::k(BL);
     const FineLevel& L = a.lv[I];
-    const int runs_parent = (I == 0) ? 1 : a.lv[I > 0 ? I - 1 : 0].runs;
+    const int runs_parent = lc.runs[BL];
     auto child = [&](int q) {
       const int j = jp + q * runs_parent;
       double S[8];
-      level_step<K>(fsm + L.xs_off + j * K * kPad + c.t, c.as + L.as_off, K, c, Sp, S);
+      if constexpr (BL == 0 && LeafCache<BT>::C4) {  // K = 4: one DMMA step, B fragments cached
+        const double af = fsm[L.xs_off + (j * 4 + c.tg) * kPad + c.t];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, lc.b4[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+      } else {
+        level_step<K>(fsm + L.xs_off + j * K * kPad + c.t, c.as + L.as_off, K, c, Sp, S);
+      }
       bot_level<NF, BL + 1, BT, G, STY>(a, S, j, c, lc);
     };
     if constexpr (I == 0) {
@@ -451,7 +472,7 @@ __device__ __forceinline__ void bot_level(const FineArgs& a, const double (&Sp)[
 
 template <int NF, class BT>
 __device__ __forceinline__ void bot_dispatch(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
-                                             const LeafCache<BT::kleaf()>& lc) {
+                                             const LeafCache<BT>& lc) {
   const bool sty = a.Y != nullptr;
   switch (a.fk) {
     case -1: sty ? bot_level<NF, 0, BT, 0, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 0, false>(a, Sp, jp, c, lc); break;
@@ -468,14 +489,14 @@ __device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S
     double v = a.fk == 1 ? gsum8<2>(S, a.fp0) : (a.fk == 2 ? gsum8<3>(S, a.fp0) : gsum8<1>(S, a.fp0));
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (c.tg == 0) fsm[a.acc_off + j * kBundle + c.t] += v;
+    if (c.tg == 0) red_add_shared(fsm + a.acc_off + j * kBundle + c.t, v);
   }
 }
 
 // Upper fine levels: runtime fans / K, register stack; hands over to the bottom block.
 template <int I, int NF, class BT>
 __device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
-                                           const LeafCache<BT::kleaf()>& lc) {
+                                           const LeafCache<BT>& lc) {
   if constexpr (BT::NB > 0 && I == NF - BT::NB) {
     bot_dispatch<NF, BT>(a, Sp, jp, c, lc);
   } else if constexpr (I >= NF) {
@@ -510,12 +531,23 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
     double* xs = fsm + L.xs_off;
-    const int per_run = kBundle * L.K;
-    for (int e = tid; e < L.runs * per_run; e += kFineThreads) {
-      const int j = e / per_run, rem = e - j * per_run, t = rem / L.K, q = rem - t * L.K;
-      double v = 0.0;
-      if (t < c.beff) v = L.X[(c.r0 + t + (int64_t)j * a.Mroot) * L.ldx + q];
-      xs[(j * L.K + q) * kPad + t] = v;
+    // lane = t (conflict-free smem stores), loop over (run, q) rows, 4 loads in flight per thread
+    const int nrow = L.runs * L.K;
+    const int t = tid & (kBundle - 1);
+    const double* src = L.X + (c.r0 + t) * L.ldx;
+    for (int r = tid >> 5; r < nrow; r += 4 * (kFineThreads >> 5)) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = r + u * (kFineThreads >> 5);
+        const int j = rr / L.K, q = rr - j * L.K;
+        v[u] = (rr < nrow && t < c.beff) ? src[(int64_t)j * a.Mroot * L.ldx + q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = r + u * (kFineThreads >> 5);
+        if (rr < nrow) xs[rr * kPad + t] = v[u];
+      }
     }
   }
   if (a.fk >= 0)
@@ -585,7 +617,17 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
         Sroot[2 * cf + 1] = p.y;
       }
     }
-    LeafCache<BT::kleaf()> lc;
+    LeafCache<BT> lc;
+#pragma unroll
+    for (int bl = 0; bl < 3; ++bl) {
+      const int I = NF - BT::NB + bl;
+      lc.runs[bl] = (I <= 0 || bl >= BT::NB) ? 1 : a.lv[I - 1].runs;
+    }
+    if constexpr (LeafCache<BT>::C4) {
+      const FineLevel& L = a.lv[NF - 3];
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) lc.b4[cf] = c.as[L.as_off + c.tg * kPad + cf * 8 + c.g];
+    }
     if constexpr (BT::NB > 0 && BT::kleaf() <= 2) {
       const FineLevel& L = a.lv[NF - 1];
 #pragma unroll
