@@ -374,17 +374,14 @@ template <class BT>
 struct LeafCache {
   static constexpr int KL = BT::kleaf();
   static constexpr bool CL = BT::NB > 0 && KL <= 2;
-  static constexpr bool C4 = BT::NB == 3 && BT::k(0) == 4;
+  // non-leaf bottom levels with K <= 4 run as ONE DMMA k-step (zero-padded to 4 when K < 4):
+  // their B fragments B[tg][g] = (tg < K ? A_w[tg][cf*8+g] : 0) are cached here
+  __host__ __device__ static constexpr bool cached(int bl) { return bl < BT::NB - 1 && BT::k(bl) <= 4; }
   double v[CL ? KL : 1][8];
-  double b4[4];
+  double bk[BT::NB > 1 ? BT::NB - 1 : 1][4];
   int runs[3];
 };
 
-// Non-returning shared-memory add (red.shared.add.f64): each rowacc slot is updated by exactly one
-// lane per column tile, so the accumulation order stays fixed (deterministic).
-__device__ __forceinline__ void red_add_shared(double* p, double v) {
-  asm volatile("red.shared.add.f64 [%0], %1;\n" ::"r"(smem_u32(p)), "d"(v) : "memory");
-}
 
 // Leaf level of the bottom block: F children of the parent tile Sp; Y store + g, batched row sums.
 template <int NF, class BT, int G, bool STY>
@@ -393,7 +390,11 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
   constexpr int BL = BT::NB - 1, I = NF - 1, F = BT::fan(BL), K = BT::k(BL);
   const FineLevel& L = a.lv[I];
   const int runs_parent = lc.runs[BL];
-  double v[F];
+  double v[F], pre[F];
+  if constexpr (G > 0 && I > 0) {  // prefetch this lane's row sums of the F leaves (hides LDS latency)
+#pragma unroll
+    for (int q = 0; q < F; ++q) pre[q] = fsm[a.acc_off + (jp + q * runs_parent) * kBundle + c.t];
+  }
   auto leaf = [&](int q) {
     const int j = jp + q * runs_parent;
     const double* xs = fsm + L.xs_off + j * K * kPad + c.t;
@@ -425,7 +426,7 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
         double s = v[q];
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (c.tg == 0) red_add_shared(fsm + a.acc_off + q * kBundle + c.t, s);
+        if (c.tg == 0) fsm[a.acc_off + q * kBundle + c.t] += s;
       }
     } else {
 #pragma unroll
@@ -434,7 +435,7 @@ __device__ __forceinline__ void bot_leaves(const FineArgs& a, const double (&Sp)
       for (int q = 0; q < F; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
       if (c.tg == 0) {
 #pragma unroll
-        for (int q = 0; q < F; ++q) red_add_shared(fsm + a.acc_off + (jp + q * runs_parent) * kBundle + c.t, v[q]);
+        for (int q = 0; q < F; ++q) fsm[a.acc_off + (jp + q * runs_parent) * kBundle + c.t] = pre[q] + v[q];
       }
     }
   }
@@ -452,10 +453,10 @@ __device__ __forceinline__ void bot_level(const FineArgs& a, const double (&Sp)[
     auto child = [&](int q) {
       const int j = jp + q * runs_parent;
       double S[8];
-      if constexpr (BL == 0 && LeafCache<BT>::C4) {  // K = 4: one DMMA step, B fragments cached
-        const double af = fsm[L.xs_off + (j * 4 + c.tg) * kPad + c.t];
+      if constexpr (LeafCache<BT>::cached(BL)) {  // K <= 4: one DMMA step, B fragments cached
+        const double af = (K == 4 || c.tg < K) ? fsm[L.xs_off + (j * K + c.tg) * kPad + c.t] : 0.0;
 #pragma unroll
-        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, lc.b4[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, lc.bk[BL][cf], Sp[2 * cf], Sp[2 * cf + 1]);
       } else {
         level_step<K>(fsm + L.xs_off + j * K * kPad + c.t, c.as + L.as_off, K, c, Sp, S);
       }
@@ -489,7 +490,7 @@ __device__ __forceinline__ void fine_consume(const FineArgs& a, const double (&S
     double v = a.fk == 1 ? gsum8<2>(S, a.fp0) : (a.fk == 2 ? gsum8<3>(S, a.fp0) : gsum8<1>(S, a.fp0));
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
-    if (c.tg == 0) red_add_shared(fsm + a.acc_off + j * kBundle + c.t, v);
+    if (c.tg == 0) fsm[a.acc_off + j * kBundle + c.t] += v;
   }
 }
 
@@ -623,10 +624,14 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
       const int I = NF - BT::NB + bl;
       lc.runs[bl] = (I <= 0 || bl >= BT::NB) ? 1 : a.lv[I - 1].runs;
     }
-    if constexpr (LeafCache<BT>::C4) {
-      const FineLevel& L = a.lv[NF - 3];
 #pragma unroll
-      for (int cf = 0; cf < 4; ++cf) lc.b4[cf] = c.as[L.as_off + c.tg * kPad + cf * 8 + c.g];
+    for (int bl = 0; bl + 1 < BT::NB; ++bl) {
+      if (LeafCache<BT>::cached(bl)) {
+        const FineLevel& L = a.lv[NF - BT::NB + bl];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf)
+          lc.bk[bl][cf] = c.tg < BT::k(bl) ? c.as[L.as_off + c.tg * kPad + cf * 8 + c.g] : 0.0;
+      }
     }
     if constexpr (BT::NB > 0 && BT::kleaf() <= 2) {
       const FineLevel& L = a.lv[NF - 1];
