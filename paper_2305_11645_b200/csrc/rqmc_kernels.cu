@@ -15,6 +15,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "rqmc_internal.h"
 
 namespace rqmc {
@@ -326,12 +328,24 @@ __device__ __forceinline__ void level_step(const double* xs, const double* as, i
       for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, aq[cf * 8], Sp[2 * cf], Sp[2 * cf + 1]);
     }
     kk = 4;
-#pragma unroll 2
-    for (; kk + 4 <= K; kk += 4) {
-      const double af = xs[(kk + c.tg) * kPad];
-      const double* aq = as + (kk + c.tg) * kPad + c.g;
+    if (kk + 4 <= K) {  // fragments of step k+4 are loaded before the DMMAs of step k issue
+      double af = xs[(kk + c.tg) * kPad], bf[4];
 #pragma unroll
-      for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, aq[cf * 8], S[2 * cf], S[2 * cf + 1]);
+      for (int cf = 0; cf < 4; ++cf) bf[cf] = as[(kk + c.tg) * kPad + c.g + cf * 8];
+      for (; kk + 8 <= K; kk += 4) {
+        const double afn = xs[(kk + 4 + c.tg) * kPad];
+        double bfn[4];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) bfn[cf] = as[(kk + 4 + c.tg) * kPad + c.g + cf * 8];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], S[2 * cf], S[2 * cf + 1]);
+        af = afn;
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) bf[cf] = bfn[cf];
+      }
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], S[2 * cf], S[2 * cf + 1]);
+      kk += 4;
     }
   } else {
     const double x = xs[0];
@@ -471,10 +485,83 @@ __device__ __forceinline__ void bot_level(const FineArgs& a, const double (&Sp)[
   }
 }
 
+// Hand-scheduled bottom block for the hot shape BotB2 (levels K = 4, 2, 1 with fans 2, i.e. b = 2 and
+// w_j = floor(log2 j)): one level-2 node -> 2 level-1 tiles -> 4 leaves.  All operand loads of the
+// node are issued first, then the DMMAs (level 2, both level-1 tiles), then the 4 leaves' DFMA +
+// g sums, then the interleaved row-sum shuffles -- so smem, DMMA, DFMA and SHFL latencies overlap
+// inside one warp.  Same arithmetic (and rounding) as the generic template path.
+template <int NF, int G, bool STY>
+__device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8], int j3, const FineCtx& c,
+                                       const LeafCache<BotB2>& lc) {
+  const FineLevel& L2 = a.lv[NF - 3];
+  const FineLevel& L1 = a.lv[NF - 2];
+  const FineLevel& L0 = a.lv[NF - 1];
+  const int r2 = lc.runs[0], r1 = lc.runs[1], r0 = lc.runs[2];
+  auto node = [&](int q2) {
+    const int j2 = j3 + q2 * r2;
+    const int j1[2] = {j2, j2 + r1};
+    const int jl[4] = {j1[0], j1[0] + r0, j1[1], j1[1] + r0};
+    // ---- operand loads of the whole node
+    const double x2 = fsm[L2.xs_off + (j2 * 4 + c.tg) * kPad + c.t];
+    double x1[2], x0[4], pre[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) x1[h] = c.tg < 2 ? fsm[L1.xs_off + (j1[h] * 2 + c.tg) * kPad + c.t] : 0.0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) x0[l] = fsm[L0.xs_off + jl[l] * kPad + c.t];
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) pre[l] = fsm[a.acc_off + jl[l] * kBundle + c.t];
+    }
+    // ---- level 2 (K = 4) and both level-1 tiles (K = 2, zero-padded k-step) on the tensor pipe
+    double S2[8], S1[2][8];
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf) dmma_c(S2[2 * cf], S2[2 * cf + 1], x2, lc.bk[0][cf], S3[2 * cf], S3[2 * cf + 1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf)
+        dmma_c(S1[h][2 * cf], S1[h][2 * cf + 1], x1[h], lc.bk[1][cf], S2[2 * cf], S2[2 * cf + 1]);
+    // ---- leaves (K = 1): y = S1 + x0 a0 (DFMA), then store / g sums
+    double v[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      double Y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) Y[e] = fma(x0[l], lc.v[0][e], S1[l >> 1][e]);
+      store_leaf<STY>(a, Y, jl[l], c);
+      if constexpr (G > 0) v[l] = gsum8<G>(Y, a.fp0);
+    }
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] += __shfl_xor_sync(0xffffffffu, v[l], 1);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] += __shfl_xor_sync(0xffffffffu, v[l], 2);
+      if (c.tg == 0) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) fsm[a.acc_off + jl[l] * kBundle + c.t] = pre[l] + v[l];
+      }
+    }
+  };
+  if (NF - 3 == 0) {
+    node(c.grp);  // the node level is the top fine level: one node per group
+  } else {
+    node(0);
+    node(1);
+  }
+}
+
 template <int NF, class BT>
 __device__ __forceinline__ void bot_dispatch(const FineArgs& a, const double (&Sp)[8], int jp, const FineCtx& c,
                                              const LeafCache<BT>& lc) {
   const bool sty = a.Y != nullptr;
+  if constexpr (std::is_same<BT, BotB2>::value) {
+    switch (a.fk) {
+      case -1: sty ? bot_b2<NF, 0, true>(a, Sp, jp, c, lc) : bot_b2<NF, 0, false>(a, Sp, jp, c, lc); return;
+      case 1: sty ? bot_b2<NF, 2, true>(a, Sp, jp, c, lc) : bot_b2<NF, 2, false>(a, Sp, jp, c, lc); return;
+      case 2: sty ? bot_b2<NF, 3, true>(a, Sp, jp, c, lc) : bot_b2<NF, 3, false>(a, Sp, jp, c, lc); return;
+      default: sty ? bot_b2<NF, 1, true>(a, Sp, jp, c, lc) : bot_b2<NF, 1, false>(a, Sp, jp, c, lc); return;
+    }
+  }
   switch (a.fk) {
     case -1: sty ? bot_level<NF, 0, BT, 0, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 0, false>(a, Sp, jp, c, lc); break;
     case 1: sty ? bot_level<NF, 0, BT, 2, true>(a, Sp, jp, c, lc) : bot_level<NF, 0, BT, 2, false>(a, Sp, jp, c, lc); break;
