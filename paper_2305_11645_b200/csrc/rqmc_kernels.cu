@@ -15,6 +15,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "rqmc_internal.h"
@@ -497,13 +498,13 @@ __device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8],
   const FineLevel& L1 = a.lv[NF - 2];
   const FineLevel& L0 = a.lv[NF - 1];
   const int r2 = lc.runs[0], r1 = lc.runs[1], r0 = lc.runs[2];
-  auto node = [&](int q2) {
+  // one level-2 node: loads, DMMAs (level 2 and both level-1 tiles), leaves -> per-leaf g sums v[]
+  auto node = [&](int q2, int (&jl)[4], double (&v)[4], double (&pre)[4]) {
     const int j2 = j3 + q2 * r2;
     const int j1[2] = {j2, j2 + r1};
-    const int jl[4] = {j1[0], j1[0] + r0, j1[1], j1[1] + r0};
-    // ---- operand loads of the whole node
+    jl[0] = j1[0]; jl[1] = j1[0] + r0; jl[2] = j1[1]; jl[3] = j1[1] + r0;
     const double x2 = fsm[L2.xs_off + (j2 * 4 + c.tg) * kPad + c.t];
-    double x1[2], x0[4], pre[4];
+    double x1[2], x0[4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) x1[h] = c.tg < 2 ? fsm[L1.xs_off + (j1[h] * 2 + c.tg) * kPad + c.t] : 0.0;
 #pragma unroll
@@ -512,7 +513,6 @@ __device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8],
 #pragma unroll
       for (int l = 0; l < 4; ++l) pre[l] = fsm[a.acc_off + jl[l] * kBundle + c.t];
     }
-    // ---- level 2 (K = 4) and both level-1 tiles (K = 2, zero-padded k-step) on the tensor pipe
     double S2[8], S1[2][8];
 #pragma unroll
     for (int cf = 0; cf < 4; ++cf) dmma_c(S2[2 * cf], S2[2 * cf + 1], x2, lc.bk[0][cf], S3[2 * cf], S3[2 * cf + 1]);
@@ -521,8 +521,6 @@ __device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8],
 #pragma unroll
       for (int cf = 0; cf < 4; ++cf)
         dmma_c(S1[h][2 * cf], S1[h][2 * cf + 1], x1[h], lc.bk[1][cf], S2[2 * cf], S2[2 * cf + 1]);
-    // ---- leaves (K = 1): y = S1 + x0 a0 (DFMA), then store / g sums
-    double v[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       double Y[8];
@@ -531,6 +529,9 @@ __device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8],
       store_leaf<STY>(a, Y, jl[l], c);
       if constexpr (G > 0) v[l] = gsum8<G>(Y, a.fp0);
     }
+  };
+  // row sums of a node's 4 leaves: butterfly over the 4 lanes of a row, then one store per row
+  auto finish = [&](const int (&jl)[4], double (&v)[4], const double (&pre)[4]) {
     if constexpr (G > 0) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) v[l] += __shfl_xor_sync(0xffffffffu, v[l], 1);
@@ -542,11 +543,16 @@ __device__ __forceinline__ void bot_b2(const FineArgs& a, const double (&S3)[8],
       }
     }
   };
-  if (NF - 3 == 0) {
-    node(c.grp);  // the node level is the top fine level: one node per group
-  } else {
-    node(0);
-    node(1);
+  int jla[4], jlb[4];
+  double va[4], vb[4], pa[4], pb[4];
+  if (NF - 3 == 0) {  // the node level is the top fine level: one node per group
+    node(c.grp, jla, va, pa);
+    finish(jla, va, pa);
+  } else {            // two sibling nodes, the first node's shuffles overlap the second's math
+    node(0, jla, va, pa);
+    node(1, jlb, vb, pb);
+    finish(jla, va, pa);
+    finish(jlb, vb, pb);
   }
 }
 
@@ -796,7 +802,359 @@ static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, cudaStream_t st)
   return launch_fine_t<NF, BotNone>(a, nb, st);
 }
 
+// ------------------------------------------------------------------------------------------
+// k_fine_tree<NF, B, G, STY>: the fused fine levels for the paper's own level shape
+// w_j = floor(log_B j) (every BASELINE config): fine level i (coarse -> fine) is
+// w = NF-1-i with K_i = (B-1) B^{NF-1-i} coordinates, every node has B children, and the fine
+// coordinates are the prefix j < B^NF - 1 of A.  With the whole tree compile-time, every loop is
+// unrolled and every smem offset is a constant; the lane/warp/CTA mapping, the smem layout and the
+// arithmetic are exactly those of k_fine (same fragments, same summation order).
+// ------------------------------------------------------------------------------------------
+template <int NF, int B>
+struct Tree {
+  __host__ __device__ static constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+  __host__ __device__ static constexpr int K(int i) { return (B - 1) * ipow(B, NF - 1 - i); }          // s_w, w = NF-1-i
+  __host__ __device__ static constexpr int runs(int i) { return ipow(B, i + 1); }                      // runs per bundle
+  static constexpr int J = ipow(B, NF) - 1;                                        // fine A rows
+  __host__ __device__ static constexpr int jlo(int i) { return ipow(B, NF - 1 - i) - 1; }              // first A row
+  static constexpr int ABUF = J * kPad;                                            // one A slab
+  static constexpr int ROOT = 2 * ABUF;                                            // root tiles
+  static constexpr int XS = ROOT + 2 * kBundle * kPad;                             // X subtree
+  static constexpr int XL = (B - 1) * ipow(B, NF) * kPad;                          // X per level
+  static constexpr int ACC = XS + NF * XL;                                         // rowacc
+  static constexpr int LEAVES = ipow(B, NF);
+  static constexpr int SMEM = (ACC + LEAVES * kBundle) * 8;
+};
+
+// S = Sp + X^red[run j] A_w, compile-time K (DMMA k-steps of 4, DFMA remainder); xs, as: level bases.
+template <int K>
+__device__ __forceinline__ void tree_step(const double* xs, const double* as, const FineCtx& c, const double (&Sp)[8],
+                                          double (&S)[8]) {
+  static_assert(K >= 1, "");
+  if constexpr (K >= 4) {
+    constexpr int NS = K / 4;
+    double af = xs[c.tg * kPad], bf[4];
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf) bf[cf] = as[c.tg * kPad + c.g + cf * 8];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {  // fragments of step s+1 are loaded before step s's DMMAs issue
+      double afn = 0.0, bfn[4] = {0.0, 0.0, 0.0, 0.0};
+      if (s + 1 < NS) {
+        afn = xs[(4 * (s + 1) + c.tg) * kPad];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) bfn[cf] = as[(4 * (s + 1) + c.tg) * kPad + c.g + cf * 8];
+      }
+      if (s == 0) {
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+      } else {
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], S[2 * cf], S[2 * cf + 1]);
+      }
+      af = afn;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) bf[cf] = bfn[cf];
+    }
+  }
+#pragma unroll
+  for (int kk = (K / 4) * 4; kk < K; ++kk) {
+    const double x = xs[kk * kPad];
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf) {
+      const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + cf * 8 + 2 * c.tg);
+      if (K < 4 && kk == 0) {
+        S[2 * cf] = fma(x, p.x, Sp[2 * cf]);
+        S[2 * cf + 1] = fma(x, p.y, Sp[2 * cf + 1]);
+      } else {
+        S[2 * cf] = fma(x, p.x, S[2 * cf]);
+        S[2 * cf + 1] = fma(x, p.y, S[2 * cf + 1]);
+      }
+    }
+  }
+}
+
+template <int NF, int B, int G, bool STY>
+struct TreeRun {
+  using T = Tree<NF, B>;
+  const FineArgs& a;
+  const FineCtx& c;
+  double a0[T::K(NF - 1) <= 2 ? T::K(NF - 1) : 1][8];  // leaf A values (K <= 2: DFMA leaves)
+  double bk[4];                                         // B fragments of a K < 4 non-leaf level (B = 2)
+
+  __device__ __forceinline__ TreeRun(const FineArgs& a_, const FineCtx& c_) : a(a_), c(c_) {}
+
+  __device__ __forceinline__ const double* xs(int i, int j) const {
+    return fsm + T::XS + i * T::XL + j * T::K(i) * kPad + c.t;
+  }
+  __device__ __forceinline__ const double* as(int i) const { return c.as + T::jlo(i) * kPad; }
+
+  // leaves of parent run jp (level NF-1): values, Y store, g sums, row-sum shuffles, rowacc update
+  __device__ __forceinline__ void leaves(const double (&Sp)[8], int jp) {
+    constexpr int I = NF - 1, KL = T::K(I), RP = T::runs(I) / B;
+    double v[B], pre[B];
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int q = 0; q < B; ++q) pre[q] = fsm[T::ACC + (jp + q * RP) * kBundle + c.t];
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int j = jp + q * RP;
+      double Y[8];
+      if constexpr (KL <= 2) {
+        const double* x = xs(I, j);
+        const double x0 = x[0];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) Y[e] = fma(x0, a0[0][e], Sp[e]);
+        if constexpr (KL == 2) {
+          const double x1 = x[kPad];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) Y[e] = fma(x1, a0[KL - 1][e], Y[e]);
+        }
+      } else {
+        tree_step<KL>(xs(I, j), as(I), c, Sp, Y);
+      }
+      store_leaf<STY>(a, Y, j, c);
+      if constexpr (G > 0) v[q] = gsum8<G>(Y, a.fp0);
+    }
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int q = 0; q < B; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 1);
+#pragma unroll
+      for (int q = 0; q < B; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
+      if (c.tg == 0) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) fsm[T::ACC + (jp + q * RP) * kBundle + c.t] = pre[q] + v[q];
+      }
+    }
+  }
+
+  template <int I>
+  __device__ __forceinline__ void level(const double (&Sp)[8], int jp) {
+    if constexpr (I == NF - 1) {
+      leaves(Sp, jp);
+    } else {
+      constexpr int RP = (I == 0) ? 1 : T::runs(I) / B;
+      auto child = [&](int q) {
+        const int j = jp + q * RP;
+        double S[8];
+        if constexpr (B == 2 && T::K(I) < 4) {  // K = 2 non-leaf level: one zero-padded DMMA step
+          const double af = c.tg < T::K(I) ? xs(I, j)[c.tg * kPad] : 0.0;
+#pragma unroll
+          for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bk[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+        } else {
+          tree_step<T::K(I)>(xs(I, j), as(I), c, Sp, S);
+        }
+        level<I + 1>(S, j);
+      };
+      if constexpr (I == 0) {
+        for (int q = c.grp; q < B; q += 2) child(q);  // top level split over the two warp groups
+      } else {
+#pragma unroll
+        for (int q = 0; q < B; ++q) child(q);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void tile(const double (&Sroot)[8]) {
+    constexpr int KL = T::K(NF - 1);
+    if constexpr (KL <= 2) {
+#pragma unroll
+      for (int q = 0; q < KL; ++q)
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) {
+          const double2 p = *reinterpret_cast<const double2*>(as(NF - 1) + q * kPad + cf * 8 + 2 * c.tg);
+          a0[q][2 * cf] = p.x;
+          a0[q][2 * cf + 1] = p.y;
+        }
+    }
+    if constexpr (B == 2 && NF >= 2) {
+      constexpr int I1 = NF - 2;  // the K = 2 level
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) bk[cf] = c.tg < T::K(I1) ? as(I1)[c.tg * kPad + cf * 8 + c.g] : 0.0;
+    }
+    level<0>(Sroot, 0);
+  }
+};
+
+template <int NF, int B, int G, bool STY>
+__global__ void __launch_bounds__(kFineThreads, 1) k_fine_tree(const FineArgs a) {
+  using T = Tree<NF, B>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  FineCtx c;
+  c.grp = warp >> 2;
+  c.wm = warp & 3;
+  c.g = lane >> 2;
+  c.tg = lane & 3;
+  c.t = c.wm * 8 + c.g;
+  c.r0 = (int64_t)blockIdx.x * kBundle;
+  c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
+
+  // X^red of the subtree -> smem [level][run][q][t]; lane = t, rows (run, q) strided over warps
+  {
+    const int t = tid & (kBundle - 1);
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      const int K = T::K(i), nrow = T::runs(i) * K;
+      const double* src = a.lv[i].X + (c.r0 + t) * (int64_t)K;
+      double* dst = fsm + T::XS + i * T::XL + t;
+      for (int r = tid >> 5; r < nrow; r += 4 * (kFineThreads >> 5)) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = r + u * (kFineThreads >> 5);
+          const int j = rr / K, q = rr - j * K;
+          v[u] = (rr < nrow && t < c.beff) ? src[(int64_t)j * a.Mroot * K + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = r + u * (kFineThreads >> 5);
+          if (rr < nrow) dst[rr * kPad] = v[u];
+        }
+      }
+    }
+  }
+  if constexpr (G > 0)
+    for (int e = tid; e < T::LEAVES * kBundle; e += kFineThreads) fsm[T::ACC + e] = 0.0;
+
+  // column tile operands (cp.async, double buffer): A rows [0, J) x 32 columns and the root tile
+  const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
+  auto load_tile = [&](int buf, int c0) {
+    double* as = fsm + buf * T::ABUF;
+    if (a.a_vec) {
+      for (int e = tid; e < T::J * (kFineBN / 2); e += kFineThreads) {
+        const int q = e >> 4, cc = (e & 15) * 2;
+        const bool ok = c0 + cc < a.tau;
+        cp_async16(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
+      }
+    } else {
+      for (int e = tid; e < T::J * kFineBN; e += kFineThreads) {
+        const int q = e >> 5, cc = e & 31;
+        const bool ok = c0 + cc < a.tau;
+        cp_async8(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
+      }
+    }
+    double* rs = fsm + T::ROOT + buf * (kBundle * kPad);
+    for (int e = tid; e < kBundle * (kFineBN / 2); e += kFineThreads) {
+      const int t = e >> 4, cc = (e & 15) * 2;
+      const bool row_ok = a.root != nullptr && t < c.beff;
+      const double* src = a.root + (c.r0 + t) * a.ldroot + c0 + cc;
+      if (c0 + cc + 1 < a.tau || !row_ok) {
+        cp_async16(rs + t * kPad + cc, row_ok ? src : a.A, row_ok);
+      } else {
+        cp_async8(rs + t * kPad + cc, row_ok && c0 + cc < a.tau ? src : a.A, row_ok && c0 + cc < a.tau);
+        cp_async8(rs + t * kPad + cc + 1, a.A, false);
+      }
+    }
+    cp_async_commit();
+  };
+
+  load_tile(0, 0);
+  for (int ct = 0; ct < ntiles; ++ct) {
+    c.c0 = ct * kFineBN;
+    c.as = fsm + (ct & 1) * T::ABUF;
+    if (ct + 1 < ntiles) {
+      load_tile((ct + 1) & 1, (ct + 1) * kFineBN);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double Sroot[8];
+    {
+      const double* rs = fsm + T::ROOT + (ct & 1) * (kBundle * kPad) + c.t * kPad + 2 * c.tg;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) {
+        const double2 p = *reinterpret_cast<const double2*>(rs + cf * 8);
+        Sroot[2 * cf] = p.x;
+        Sroot[2 * cf + 1] = p.y;
+      }
+    }
+    TreeRun<NF, B, G, STY> run(a, c);
+    run.tile(Sroot);
+    __syncthreads();
+  }
+
+  if constexpr (G > 0) {
+    const double pad = (G == 2) ? (double)(ntiles * kFineBN - a.tau) : 0.0;
+    double part = 0.0;
+    for (int e = tid; e < T::LEAVES * kBundle; e += kFineThreads) {
+      const int t = e % kBundle;
+      if (t >= c.beff) continue;
+      const double mean = (fsm[T::ACC + e] - pad) / a.tau;
+      double fv;
+      switch (a.fk) {
+        case 0: fv = exp(mean); break;
+        case 1: fv = mean - a.fp1; fv = fv > 0.0 ? fv : 0.0; break;
+        default: fv = mean; break;
+      }
+      part += fv;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __shared__ double red[kFineThreads / 32];
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kFineThreads / 32; ++w) t += red[w];
+      a.partial[blockIdx.x] = t;
+    }
+  }
+}
+
+template <int NF, int B, int G, bool STY>
+static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k_fine_tree<NF, B, G, STY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Tree<NF, B>::SMEM);
+  if (e != cudaSuccess) return e;
+  k_fine_tree<NF, B, G, STY><<<(unsigned)nb, kFineThreads, Tree<NF, B>::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Does the fine level table have the compile-time shape Tree<NF, B> (and the same smem layout)?
+template <int NF, int B>
+static bool tree_matches(const FineArgs& a) {
+  using T = Tree<NF, B>;
+  if (a.NF != NF || a.smem_bytes != T::SMEM || a.acc_off != T::ACC || a.leafruns != T::LEAVES) return false;
+  for (int i = 0; i < NF; ++i) {
+    const FineLevel& L = a.lv[i];
+    if (L.K != T::K(i) || L.fan != B || L.runs != T::runs(i) || L.j_lo != T::jlo(i) || L.ldx != L.K ||
+        L.xs_off != T::XS + i * T::XL)
+      return false;
+  }
+  return true;
+}
+
+template <int NF, int B>
+static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, cudaStream_t st) {
+  const bool sty = a.Y != nullptr;
+  switch (a.fk) {
+    case -1: return launch_tree_t<NF, B, 0, true>(a, nb, st);
+    case 1: return sty ? launch_tree_t<NF, B, 2, true>(a, nb, st) : launch_tree_t<NF, B, 2, false>(a, nb, st);
+    case 2: return sty ? launch_tree_t<NF, B, 3, true>(a, nb, st) : launch_tree_t<NF, B, 3, false>(a, nb, st);
+    default: return sty ? launch_tree_t<NF, B, 1, true>(a, nb, st) : launch_tree_t<NF, B, 1, false>(a, nb, st);
+  }
+}
+
+// returns cudaErrorNotSupported when no compile-time tree matches
+static cudaError_t launch_tree(const FineArgs& a, int64_t nb, cudaStream_t st) {
+  if (a.Y == nullptr && a.fk < 0) return cudaErrorNotSupported;
+  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, st);
+  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, st);
+  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, st);
+  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, st);
+  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, st);
+  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, st);
+  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, st);
+  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, st);
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_fine(const FineArgs& a, int64_t nb, cudaStream_t st) {
+  if (std::getenv("RQMC_NO_TREE") == nullptr) {
+    const cudaError_t e = launch_tree(a, nb, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (a.NF) {
     case 0: return launch_fine_t<0, BotNone>(a, nb, st);
     case 1: return launch_fine_n<1>(a, nb, st);
