@@ -810,6 +810,9 @@ static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, cudaStream_t st)
 // unrolled and every smem offset is a constant; the lane/warp/CTA mapping, the smem layout and the
 // arithmetic are exactly those of k_fine (same fragments, same summation order).
 // ------------------------------------------------------------------------------------------
+// K = 2 non-leaf level of the b = 2 tree: one zero-padded DMMA step (true) or 2 DFMA steps (false)
+constexpr bool kTreePadK2 = true;
+
 template <int NF, int B>
 struct Tree {
   __host__ __device__ static constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
@@ -928,9 +931,71 @@ struct TreeRun {
     }
   }
 
+  // b = 2 bottom (levels K = 4, 2, 1 below the parent tile Sp): both level-2 nodes (or the group's
+  // one, at the top), their level-1 tiles and all leaves are formed first, then the 8 (4) row-sum
+  // shuffle chains run together and the prefetched rowacc slots are updated once.
+  __device__ __forceinline__ void bottom_b2(const double (&Sp)[8], int jp) {
+    constexpr int I2 = NF - 3, I1 = NF - 2, I0 = NF - 1;
+    constexpr int RP2 = (I2 == 0) ? 1 : T::runs(I2) / 2, RP1 = T::runs(I1) / 2, RP0 = T::runs(I0) / 2;
+    constexpr int NQ = (I2 == 0) ? 1 : 2;  // level-2 nodes handled by this warp
+    int jl[4 * NQ];
+    double v[4 * NQ], pre[4 * NQ];
+#pragma unroll
+    for (int n = 0; n < NQ; ++n) {
+      const int q2 = (I2 == 0) ? c.grp : n;
+      const int j2 = jp + q2 * RP2;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) jl[4 * n + l] = j2 + (l >> 1) * RP1 + (l & 1) * RP0;
+    }
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int l = 0; l < 4 * NQ; ++l) pre[l] = fsm[T::ACC + jl[l] * kBundle + c.t];
+    }
+#pragma unroll
+    for (int n = 0; n < NQ; ++n) {
+      const int j2 = jl[4 * n];
+      double S2[8];
+      tree_step<4>(xs(I2, j2), as(I2), c, Sp, S2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j1 = j2 + h * RP1;
+        double S1[8];
+        if constexpr (kTreePadK2) {
+          const double af = c.tg < 2 ? xs(I1, j1)[c.tg * kPad] : 0.0;
+#pragma unroll
+          for (int cf = 0; cf < 4; ++cf) dmma_c(S1[2 * cf], S1[2 * cf + 1], af, bk[cf], S2[2 * cf], S2[2 * cf + 1]);
+        } else {
+          tree_step<2>(xs(I1, j1), as(I1), c, S2, S1);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int l = 4 * n + 2 * h + q;
+          const double x0 = xs(I0, jl[l])[0];
+          double Y[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) Y[e] = fma(x0, a0[0][e], S1[e]);
+          store_leaf<STY>(a, Y, jl[l], c);
+          if constexpr (G > 0) v[l] = gsum8<G>(Y, a.fp0);
+        }
+      }
+    }
+    if constexpr (G > 0) {
+#pragma unroll
+      for (int l = 0; l < 4 * NQ; ++l) v[l] += __shfl_xor_sync(0xffffffffu, v[l], 1);
+#pragma unroll
+      for (int l = 0; l < 4 * NQ; ++l) v[l] += __shfl_xor_sync(0xffffffffu, v[l], 2);
+      if (c.tg == 0) {
+#pragma unroll
+        for (int l = 0; l < 4 * NQ; ++l) fsm[T::ACC + jl[l] * kBundle + c.t] = pre[l] + v[l];
+      }
+    }
+  }
+
   template <int I>
   __device__ __forceinline__ void level(const double (&Sp)[8], int jp) {
-    if constexpr (I == NF - 1) {
+    if constexpr (B == 2 && NF >= 3 && I == NF - 3) {
+      bottom_b2(Sp, jp);
+    } else if constexpr (I == NF - 1) {
       leaves(Sp, jp);
     } else {
       constexpr int RP = (I == 0) ? 1 : T::runs(I) / B;
