@@ -1,0 +1,116 @@
+// Device helpers shared by the sm_100a kernel translation units (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "rqmc_internal.h"
+
+namespace rqmc {
+
+// ------------------------------------------------------------------------------------------
+// async copy helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// DMMA.8x8x4: D(8x8) += A(8x4, row) B(4x8, col); lane l: a = A[l/4][l%4], b = B[l%4][l/4],
+// d = {D[l/4][2(l%4)], D[l/4][2(l%4)+1]}
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------------------------------
+// a3+a4+a5: fused fine levels.  CTA = bundle of kBundle (32) residues of the checkpoint level x a
+// kFineBN (32)-column tile, 8 warps in two groups; group h walks the subtrees under the top fine
+// level's runs q = h (mod 2), so the two groups never touch the same leaf row.  In a group, warp
+// wm owns rows 8 wm .. 8 wm + 7 of every run and all 32 columns = 1 x 4 DMMA.8x8x4 fragments, so a
+// path tile is 8 doubles per lane and one lane's 8 leaf values share ONE row (cheap row sums).
+// The DFS stack (one tile per fine level) lives in registers.  K >= 4 steps run on the fp64 tensor
+// pipe (mma.sync f64 with C and D in different registers: no stack copies), K mod 4 remainders and
+// K < 4 levels as DFMA on the same fragment registers (no zero padding).
+// The bottom NB levels of common shapes (BT) are compile-time: fans and K known, loops unrolled,
+// leaf consumption (Y store, g) templated, so the per-leaf control overhead disappears.
+// Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36 doubles
+// (bank-conflict-free fragment loads).  Columns >= tau are zero in the A slab and the root tile, so
+// leaf values there are exactly 0 and need no mask (g = exp is corrected in the finalisation).
+// ------------------------------------------------------------------------------------------
+constexpr int kPad = kFinePad;
+
+struct FineCtx {
+  int grp, wm, g, tg, t, beff, c0;
+  int64_t r0;
+  const double* as;      // A slab of the current column tile
+};
+
+// D = A B + C with C and D in distinct registers (DMMA.8x8x4)
+__device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+extern __shared__ __align__(16) double fsm[];  // dynamic smem of the fine kernels
+
+// ---- g kinds (f(y) = F(tau^-1 sum_c g(y_c)), reading C-17): 0 none, 1 identity, 2 exp(p0 y), 3 y^2
+template <int G>
+__device__ __forceinline__ double gsum8(const double (&S)[8], double p0) {
+  if constexpr (G == 2) {
+    double v = exp(p0 * S[0]);
+#pragma unroll
+    for (int e = 1; e < 8; ++e) v += exp(p0 * S[e]);
+    return v;
+  } else if constexpr (G == 3) {
+    double v = S[0] * S[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) v = fma(S[e], S[e], v);
+    return v;
+  } else {
+    return ((S[0] + S[1]) + (S[2] + S[3])) + ((S[4] + S[5]) + (S[6] + S[7]));
+  }
+}
+
+// F(mean) of f(y) = F(tau^-1 sum_c g(y_c)) (reading C-17): fk 0 exp, 1 max(. - p1, 0), else identity
+__device__ __forceinline__ double f_of_mean(const FineArgs& a, double mean) {
+  switch (a.fk) {
+    case 0: return exp(mean);
+    case 1: { const double v = mean - a.fp1; return v > 0.0 ? v : 0.0; }
+    default: return mean;
+  }
+}
+
+template <bool STY>
+__device__ __forceinline__ void store_leaf(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
+  if constexpr (STY) {
+    if (c.t < c.beff) {
+      double* yr = a.Y + (c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) {
+        const int col = c.c0 + cf * 8 + 2 * c.tg;
+        if (col + 1 < a.tau) {
+          if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(S[2 * cf], S[2 * cf + 1]);
+          else { yr[col] = S[2 * cf]; yr[col + 1] = S[2 * cf + 1]; }
+        } else if (col < a.tau) {
+          yr[col] = S[2 * cf];
+        }
+      }
+    }
+  }
+}
+
+
+}  // namespace rqmc
