@@ -1,4 +1,7 @@
-// k_fine_tree: compile-time fused fine levels for the paper's level shape w_j = floor(log_b j).
+// k_fine_tree: compile-time fused fine levels for the paper's level shape w_j = floor(log_b j)
+// (every BASELINE config).  Rows a3+a4+a5 of SURVEY §8(a): Alg. 2's recursion
+// R_w[r] = P_w[r] + R_w'[r mod M_w'] walked depth-first below one bundle of checkpoint
+// residues, fused with the leaf consumption (Y store and/or F(tau^-1 sum_c g(y_c))).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -11,74 +14,96 @@
 namespace rqmc {
 
 // ------------------------------------------------------------------------------------------
-// k_fine_tree<NF, B, G, STY>: the fused fine levels for the paper's own level shape
-// w_j = floor(log_B j) (every BASELINE config): fine level i (coarse -> fine) is
-// w = NF-1-i with K_i = (B-1) B^{NF-1-i} coordinates, every node has B children, and the fine
-// coordinates are the prefix j < B^NF - 1 of A.  With the whole tree compile-time, every loop is
-// unrolled and every smem offset is a constant; the lane/warp/CTA mapping, the smem layout and the
-// arithmetic are exactly those of k_fine (same fragments, same summation order).
+// k_fine_tree<NF, B, G, STY, NFR>.  Fine level i (coarse -> fine) is w = NF-1-i with
+// K_i = (B-1) B^{NF-1-i} coordinates, every node has B children, and the fine coordinates are the
+// prefix j < B^NF - 1 of A.  With the whole tree compile-time every loop is unrolled and every
+// smem offset is a constant.
+//
+// CTA = one bundle of 32 checkpoint residues x one 32-column tile at a time (64 tiles for tau =
+// 2048), 2 warp groups (group h walks the subtrees under the top level's runs q = h mod 2) x
+// 4/NFR column slices x 4 row blocks.  A warp owns 8 residues x 8 NFR columns = NFR DMMA.8x8x4
+// accumulator fragments, so a tree node is 2 NFR doubles per lane and the DFS stack lives in
+// registers.  NFR = 4 (8 warps, 255 registers) is the default; NFR = 2 (16 warps, 128 registers,
+// more LDS and shuffles per output) measured 2 % slower on C5 (20.03 vs 19.59 ms).
+//
+//   K >= 4 levels : DMMA.8x8x4 k-steps (mma.sync f64, C and D in distinct registers)
+//   K = 2 level   : 2 DFMA per output on A values cached in registers per column tile
+//   K = 1 leaves  : 1 DFMA per output, then Y store / g, lane-local sums of g
+//   row sums      : b = 2: one transpose-reduce over the 4 lanes of a row per 4 NQ leaves; each
+//                   lane keeps complete column-slice sums of its leaf rows in registers across all
+//                   column tiles (no shared-memory row accumulators); other shapes: smem rowacc.
+// Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36
+// doubles (bank-conflict-free fragment loads); columns >= tau are zero in the A slab and root tile.
 // ------------------------------------------------------------------------------------------
-// K = 2 non-leaf level of the b = 2 tree: 2 DFMA steps on cached A values (default) or, with
-// -DRQMC_K2_PAD=1, one zero-padded DMMA step (twice the fp64-pipe time, fewer issue slots)
-#ifndef RQMC_K2_PAD
-#define RQMC_K2_PAD 0
-#endif
-#ifndef RQMC_K2_CACHE          // DFMA K = 2 level: A values cached in registers per column tile (1) or read from smem
-#define RQMC_K2_CACHE 1
+#ifndef RQMC_TREE_NFR
+#define RQMC_TREE_NFR 4
 #endif
 
-template <int NF, int B>
+template <int NF, int B, int NFR>
 struct Tree {
   __host__ __device__ static constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
-  __host__ __device__ static constexpr int K(int i) { return (B - 1) * ipow(B, NF - 1 - i); }          // s_w, w = NF-1-i
-  __host__ __device__ static constexpr int runs(int i) { return ipow(B, i + 1); }                      // runs per bundle
-  static constexpr int J = ipow(B, NF) - 1;                                        // fine A rows
-  __host__ __device__ static constexpr int jlo(int i) { return ipow(B, NF - 1 - i) - 1; }              // first A row
-  static constexpr int ABUF = J * kPad;                                            // one A slab
-  static constexpr int ROOT = 2 * ABUF;                                            // root tiles
-  static constexpr int XS = ROOT + 2 * kBundle * kPad;                             // X subtree
-  static constexpr int XL = (B - 1) * ipow(B, NF) * kPad;                          // X per level
-  static constexpr int ACC = XS + NF * XL;                                         // rowacc
+  __host__ __device__ static constexpr int K(int i) { return (B - 1) * ipow(B, NF - 1 - i); }  // s_w, w = NF-1-i
+  __host__ __device__ static constexpr int runs(int i) { return ipow(B, i + 1); }              // runs per bundle
+  __host__ __device__ static constexpr int jlo(int i) { return ipow(B, NF - 1 - i) - 1; }      // first A row
+  static constexpr int J = ipow(B, NF) - 1;                        // fine A rows
+  static constexpr int CH = 4 / NFR;                               // column slices per group
+  static constexpr int WARPS = 8 * CH;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int NV = 2 * NFR;                               // doubles per lane per node
   static constexpr int LEAVES = ipow(B, NF);
-  static constexpr int SMEM = (ACC + LEAVES * kBundle) * 8;
+  static constexpr bool kRegAcc = (B == 2 && NF >= 3);             // register row sums (b = 2 bottom)
+  static constexpr int ABUF = J * kPad;                            // one A slab
+  static constexpr int ROOT = 2 * ABUF;                            // root tiles
+  static constexpr int XS = ROOT + 2 * kBundle * kPad;             // X subtree
+  static constexpr int XL = (B - 1) * ipow(B, NF) * kPad;          // X per level
+  static constexpr int ACC = XS + NF * XL;                         // rowacc [ch][leaf][t]
+  static constexpr int ACCN = kRegAcc ? 0 : CH * LEAVES * kBundle;
+  static constexpr int SMEM = (ACC + ACCN) * 8;
 };
 
-// S = Sp + X^red[run j] A_w, compile-time K (DMMA k-steps of 4, DFMA remainder); xs, as: level bases.
-template <int K>
-__device__ __forceinline__ void tree_step(const double* xs, const double* as, const FineCtx& c, const double (&Sp)[8],
-                                          double (&S)[8]) {
+struct TreeCtx {
+  int grp, ch, wm, g, tg, t, cw, beff, c0;
+  int64_t r0;
+  const double* as;  // A slab of the current column tile
+};
+
+// S = Sp + X^red[run] A_w, compile-time K (DMMA k-steps of 4, DFMA remainder); xs, as: level bases.
+template <int K, int NFR>
+__device__ __forceinline__ void tree_step(const double* xs, const double* as, const TreeCtx& c,
+                                          const double (&Sp)[2 * NFR], double (&S)[2 * NFR]) {
   static_assert(K >= 1, "");
   if constexpr (K >= 4) {
     constexpr int NS = K / 4;
-    double af = xs[c.tg * kPad], bf[4];
+    const double* ab = as + c.cw + c.g;
+    double af = xs[c.tg * kPad], bf[NFR];
 #pragma unroll
-    for (int cf = 0; cf < 4; ++cf) bf[cf] = as[c.tg * kPad + c.g + cf * 8];
+    for (int cf = 0; cf < NFR; ++cf) bf[cf] = ab[c.tg * kPad + cf * 8];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {  // fragments of step s+1 are loaded before step s's DMMAs issue
-      double afn = 0.0, bfn[4] = {0.0, 0.0, 0.0, 0.0};
+      double afn = 0.0, bfn[NFR];
+#pragma unroll
+      for (int cf = 0; cf < NFR; ++cf) bfn[cf] = 0.0;
       if (s + 1 < NS) {
         afn = xs[(4 * (s + 1) + c.tg) * kPad];
 #pragma unroll
-        for (int cf = 0; cf < 4; ++cf) bfn[cf] = as[(4 * (s + 1) + c.tg) * kPad + c.g + cf * 8];
+        for (int cf = 0; cf < NFR; ++cf) bfn[cf] = ab[(4 * (s + 1) + c.tg) * kPad + cf * 8];
       }
-      if (s == 0) {
 #pragma unroll
-        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], Sp[2 * cf], Sp[2 * cf + 1]);
-      } else {
-#pragma unroll
-        for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], S[2 * cf], S[2 * cf + 1]);
+      for (int cf = 0; cf < NFR; ++cf) {
+        if (s == 0) dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+        else dmma_c(S[2 * cf], S[2 * cf + 1], af, bf[cf], S[2 * cf], S[2 * cf + 1]);
       }
       af = afn;
 #pragma unroll
-      for (int cf = 0; cf < 4; ++cf) bf[cf] = bfn[cf];
+      for (int cf = 0; cf < NFR; ++cf) bf[cf] = bfn[cf];
     }
   }
 #pragma unroll
   for (int kk = (K / 4) * 4; kk < K; ++kk) {
     const double x = xs[kk * kPad];
 #pragma unroll
-    for (int cf = 0; cf < 4; ++cf) {
-      const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + cf * 8 + 2 * c.tg);
+    for (int cf = 0; cf < NFR; ++cf) {
+      const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + c.cw + cf * 8 + 2 * c.tg);
       if (K < 4 && kk == 0) {
         S[2 * cf] = fma(x, p.x, Sp[2 * cf]);
         S[2 * cf + 1] = fma(x, p.y, Sp[2 * cf + 1]);
@@ -90,32 +115,68 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
   }
 }
 
-template <int NF, int B, int G, bool STY>
+// lane-local sum of g over one leaf node's NV values (reading C-17: 1 identity, 2 exp(p0 y), 3 y^2)
+template <int G, int NV>
+__device__ __forceinline__ double gsum(const double (&S)[NV], double p0) {
+  if constexpr (G == 2) {
+    double v = exp(p0 * S[0]);
+#pragma unroll
+    for (int e = 1; e < NV; ++e) v += exp(p0 * S[e]);
+    return v;
+  } else if constexpr (G == 3) {
+    double v = S[0] * S[0];
+#pragma unroll
+    for (int e = 1; e < NV; ++e) v = fma(S[e], S[e], v);
+    return v;
+  } else if constexpr (NV == 8) {
+    return ((S[0] + S[1]) + (S[2] + S[3])) + ((S[4] + S[5]) + (S[6] + S[7]));
+  } else {
+    static_assert(NV == 4, "");
+    return (S[0] + S[1]) + (S[2] + S[3]);
+  }
+}
+
+template <bool STY, int NFR>
+__device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[2 * NFR], int j, const TreeCtx& c) {
+  if constexpr (STY) {
+    if (c.t < c.beff) {
+      double* yr = a.Y + (c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+#pragma unroll
+      for (int cf = 0; cf < NFR; ++cf) {
+        const int col = c.c0 + c.cw + cf * 8 + 2 * c.tg;
+        if (col + 1 < a.tau) {
+          if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(S[2 * cf], S[2 * cf + 1]);
+          else { yr[col] = S[2 * cf]; yr[col + 1] = S[2 * cf + 1]; }
+        } else if (col < a.tau) {
+          yr[col] = S[2 * cf];
+        }
+      }
+    }
+  }
+}
+
+template <int NF, int B, int G, bool STY, int NFR>
 struct TreeRun {
-  using T = Tree<NF, B>;
-  // b = 2 trees with >= 3 fine levels: the bottom three levels run as one block (bottom_b2) and the
-  // row sums of g live in registers across all column tiles (kRegAcc); otherwise in smem (rowacc).
+  using T = Tree<NF, B, NFR>;
+  static constexpr int NV = T::NV;
   static constexpr bool kB2 = (B == 2 && NF >= 3);
-  static constexpr bool kRegAcc = kB2 && G > 0;
+  static constexpr bool kRegAcc = T::kRegAcc && G > 0;
   static constexpr int I2 = NF - 3;                                // the K = 4 level of the b = 2 bottom
   static constexpr int NQ = (I2 <= 0) ? 1 : 2;                     // K = 4 nodes per bottom block
   static constexpr int NBAT = (I2 <= 0) ? 1 : T::ipow(2, I2 - 1);  // bottom blocks per warp and tile
   static constexpr int RW = NQ;                                    // leaf row sums a lane keeps per block
+  static constexpr int NACC = kRegAcc ? NBAT * RW : 1;
   static constexpr int K1 = (B == 2 && NF >= 2) ? T::K(NF - 2) : 0;  // the K = 2 level (b = 2)
 
   const FineArgs& a;
-  const FineCtx& c;
-  double a0[T::K(NF - 1) <= 2 ? T::K(NF - 1) : 1][8];  // leaf A values (K <= 2: DFMA leaves)
-#if RQMC_K2_PAD
-  double bk[4];                                         // B fragments of the zero-padded K = 2 DMMA step
-#else
-  double a1[K1 == 2 && RQMC_K2_CACHE ? 2 : 1][8];       // A values of the K = 2 level (DFMA, no padding)
-#endif
-  double racc[kRegAcc ? NBAT * RW : 1];                 // row sums sum_c g(y_kc) of this lane's leaf rows
+  const TreeCtx& c;
+  double a0[T::K(NF - 1) <= 2 ? T::K(NF - 1) : 1][NV];  // leaf A values (K <= 2: DFMA leaves)
+  double a1[K1 == 2 ? 2 : 1][NV];                       // A values of the K = 2 level (DFMA)
+  double racc[NACC];                                    // row sums sum_c g(y_kc) of this lane's leaf rows
 
-  __device__ __forceinline__ TreeRun(const FineArgs& a_, const FineCtx& c_) : a(a_), c(c_) {
+  __device__ __forceinline__ TreeRun(const FineArgs& a_, const TreeCtx& c_) : a(a_), c(c_) {
 #pragma unroll
-    for (int i = 0; i < (kRegAcc ? NBAT * RW : 1); ++i) racc[i] = 0.0;
+    for (int i = 0; i < NACC; ++i) racc[i] = 0.0;
   }
 
   __device__ __forceinline__ const double* xs(int i, int j) const {
@@ -123,48 +184,46 @@ struct TreeRun {
   }
   __device__ __forceinline__ const double* as(int i) const { return c.as + T::jlo(i) * kPad; }
 
-  // S = Sp + X^red[run j] A_w for the K = 2 level (b = 2): cached A values, DFMA (or one padded DMMA)
-  __device__ __forceinline__ void step_k2(const double (&Sp)[8], int i, int j, double (&S)[8]) const {
-#if RQMC_K2_PAD
-    const double af = c.tg < 2 ? xs(i, j)[c.tg * kPad] : 0.0;
-#pragma unroll
-    for (int cf = 0; cf < 4; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, bk[cf], Sp[2 * cf], Sp[2 * cf + 1]);
-#elif RQMC_K2_CACHE
+  // S = Sp + X^red_w[run j] A_w for the K = 2 level (b = 2): cached A values, DFMA
+  __device__ __forceinline__ void step_k2(const double (&Sp)[NV], int i, int j, double (&S)[NV]) const {
     const double x0 = xs(i, j)[0], x1 = xs(i, j)[kPad];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) S[e] = fma(x1, a1[1][e], fma(x0, a1[0][e], Sp[e]));
-#else
-    tree_step<2>(xs(i, j), as(i), c, Sp, S);
-#endif
+    for (int e = 0; e < NV; ++e) S[e] = fma(x1, a1[1][e], fma(x0, a1[0][e], Sp[e]));
+  }
+  template <int I>
+  __device__ __forceinline__ void step(const double (&Sp)[NV], int j, double (&S)[NV]) const {
+    if constexpr (B == 2 && T::K(I) == 2) step_k2(Sp, I, j, S);
+    else tree_step<T::K(I), NFR>(xs(I, j), as(I), c, Sp, S);
   }
 
-  // leaves of parent run jp (level NF-1): values, Y store, g sums, row-sum shuffles, rowacc update
-  __device__ __forceinline__ void leaves(const double (&Sp)[8], int jp) {
+  // leaves of parent run jp (level NF-1), generic shapes: Y store, g sums, smem rowacc[ch][leaf][t]
+  __device__ __forceinline__ void leaves(const double (&Sp)[NV], int jp) {
     constexpr int I = NF - 1, KL = T::K(I), RP = T::runs(I) / B;
+    double* acc = fsm + T::ACC + c.ch * (T::LEAVES * kBundle) + c.t;
     double v[B], pre[B];
     if constexpr (G > 0) {
 #pragma unroll
-      for (int q = 0; q < B; ++q) pre[q] = fsm[T::ACC + (jp + q * RP) * kBundle + c.t];
+      for (int q = 0; q < B; ++q) pre[q] = acc[(jp + q * RP) * kBundle];
     }
 #pragma unroll
     for (int q = 0; q < B; ++q) {
       const int j = jp + q * RP;
-      double Y[8];
+      double Y[NV];
       if constexpr (KL <= 2) {
         const double* x = xs(I, j);
         const double x0 = x[0];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) Y[e] = fma(x0, a0[0][e], Sp[e]);
+        for (int e = 0; e < NV; ++e) Y[e] = fma(x0, a0[0][e], Sp[e]);
         if constexpr (KL == 2) {
           const double x1 = x[kPad];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) Y[e] = fma(x1, a0[KL - 1][e], Y[e]);
+          for (int e = 0; e < NV; ++e) Y[e] = fma(x1, a0[KL - 1][e], Y[e]);
         }
       } else {
-        tree_step<KL>(xs(I, j), as(I), c, Sp, Y);
+        tree_step<KL, NFR>(xs(I, j), as(I), c, Sp, Y);
       }
-      store_leaf<STY>(a, Y, j, c);
-      if constexpr (G > 0) v[q] = gsum8<G>(Y, a.fp0);
+      tree_store<STY, NFR>(a, Y, j, c);
+      if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0);
     }
     if constexpr (G > 0) {
 #pragma unroll
@@ -173,17 +232,17 @@ struct TreeRun {
       for (int q = 0; q < B; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
       if (c.tg == 0) {
 #pragma unroll
-        for (int q = 0; q < B; ++q) fsm[T::ACC + (jp + q * RP) * kBundle + c.t] = pre[q] + v[q];
+        for (int q = 0; q < B; ++q) acc[(jp + q * RP) * kBundle] = pre[q] + v[q];
       }
     }
   }
 
   // b = 2 bottom (levels K = 4, 2, 1 below the parent tile Sp, bottom block number P of this warp):
   // the NQ level-(NF-3) nodes, their level-(NF-2) tiles and all 4 NQ leaves are formed first; then one
-  // transpose-reduce over the 4 lanes of each row leaves lane tg with the complete 32-column sums of
-  // the leaves 2 tg, 2 tg + 1 (NQ = 2; leaf tg for NQ = 1), accumulated in registers.
+  // transpose-reduce over the 4 lanes of each row leaves lane tg with the column-slice sums of the
+  // leaves 2 tg, 2 tg + 1 (NQ = 2; leaf tg for NQ = 1), accumulated in registers.
   template <int P>
-  __device__ __forceinline__ void bottom_b2(const double (&Sp)[8], int jp) {
+  __device__ __forceinline__ void bottom_b2(const double (&Sp)[NV], int jp) {
     constexpr int I1 = NF - 2, I0 = NF - 1;
     constexpr int RP2 = (I2 == 0) ? 1 : T::runs(I2) / 2, RP1 = T::runs(I1) / 2, RP0 = T::runs(I0) / 2;
     constexpr int NL = 4 * NQ;
@@ -199,21 +258,21 @@ struct TreeRun {
 #pragma unroll
     for (int n = 0; n < NQ; ++n) {
       const int j2 = jl[4 * n];
-      double S2[8];
-      tree_step<4>(xs(I2, j2), as(I2), c, Sp, S2);
+      double S2[NV];
+      tree_step<4, NFR>(xs(I2, j2), as(I2), c, Sp, S2);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        double S1[8];
+        double S1[NV];
         step_k2(S2, I1, j2 + h * RP1, S1);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int l = 4 * n + 2 * h + q;
           const double x0 = xs(I0, jl[l])[0];
-          double Y[8];
+          double Y[NV];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) Y[e] = fma(x0, a0[0][e], S1[e]);
-          store_leaf<STY>(a, Y, jl[l], c);
-          if constexpr (G > 0) v[l] = gsum8<G>(Y, a.fp0);
+          for (int e = 0; e < NV; ++e) Y[e] = fma(x0, a0[0][e], S1[e]);
+          tree_store<STY, NFR>(a, Y, jl[l], c);
+          if constexpr (G > 0) v[l] = gsum<G, NV>(Y, a.fp0);
         }
       }
     }
@@ -239,139 +298,118 @@ struct TreeRun {
   // children at level I of the parent tile Sp (run jp); P = the parent's position among this warp's
   // level-(I-1) nodes (compile time, so register row sums are statically indexed)
   template <int I, int P>
-  __device__ __forceinline__ void level(const double (&Sp)[8], int jp) {
+  __device__ __forceinline__ void level(const double (&Sp)[NV], int jp) {
     if constexpr (kB2 && I == I2) {
       bottom_b2<P>(Sp, jp);
     } else if constexpr (I == NF - 1) {
       leaves(Sp, jp);
-    } else {
-      constexpr int RP = (I == 0) ? 1 : T::runs(I) / B;
-      if constexpr (I == 0) {
-        for (int q = c.grp; q < B; q += 2) {  // top level split over the two warp groups
-          double S[8];
-          if constexpr (B == 2 && T::K(I) == 2) step_k2(Sp, I, q, S);
-          else tree_step<T::K(I)>(xs(I, q), as(I), c, Sp, S);
-          level<I + 1, 0>(S, q);
-        }
-      } else {
-        level_children<I, P, 0>(Sp, jp);
+    } else if constexpr (I == 0) {
+      for (int q = c.grp; q < B; q += 2) {  // top level split over the two warp groups
+        double S[NV];
+        step<0>(Sp, q, S);
+        level<1, 0>(S, q);
       }
+    } else {
+      level_children<I, P, 0>(Sp, jp);
     }
   }
   template <int I, int P, int Q>
-  __device__ __forceinline__ void level_children(const double (&Sp)[8], int jp) {
+  __device__ __forceinline__ void level_children(const double (&Sp)[NV], int jp) {
     if constexpr (Q < B) {
-      constexpr int RP = T::runs(I) / B;
-      const int j = jp + Q * RP;
-      double S[8];
-      if constexpr (B == 2 && T::K(I) == 2) step_k2(Sp, I, j, S);
-      else tree_step<T::K(I)>(xs(I, j), as(I), c, Sp, S);
+      const int j = jp + Q * (T::runs(I) / B);
+      double S[NV];
+      step<I>(Sp, j, S);
       level<I + 1, P * B + Q>(S, j);
       level_children<I, P, Q + 1>(Sp, jp);
     }
   }
 
-  __device__ __forceinline__ void tile(const double (&Sroot)[8]) {
+  __device__ __forceinline__ void load_cache(double (&dst)[NV], const double* row) const {
+#pragma unroll
+    for (int cf = 0; cf < NFR; ++cf) {
+      const double2 p = *reinterpret_cast<const double2*>(row + c.cw + cf * 8 + 2 * c.tg);
+      dst[2 * cf] = p.x;
+      dst[2 * cf + 1] = p.y;
+    }
+  }
+
+  __device__ __forceinline__ void tile(const double (&Sroot)[NV]) {
     constexpr int KL = T::K(NF - 1);
     if constexpr (KL <= 2) {
 #pragma unroll
-      for (int q = 0; q < KL; ++q)
-#pragma unroll
-        for (int cf = 0; cf < 4; ++cf) {
-          const double2 p = *reinterpret_cast<const double2*>(as(NF - 1) + q * kPad + cf * 8 + 2 * c.tg);
-          a0[q][2 * cf] = p.x;
-          a0[q][2 * cf + 1] = p.y;
-        }
+      for (int q = 0; q < KL; ++q) load_cache(a0[q], as(NF - 1) + q * kPad);
     }
     if constexpr (K1 == 2) {
-#if RQMC_K2_PAD
 #pragma unroll
-      for (int cf = 0; cf < 4; ++cf) bk[cf] = c.tg < 2 ? as(NF - 2)[c.tg * kPad + cf * 8 + c.g] : 0.0;
-#elif RQMC_K2_CACHE
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int cf = 0; cf < 4; ++cf) {
-          const double2 p = *reinterpret_cast<const double2*>(as(NF - 2) + q * kPad + cf * 8 + 2 * c.tg);
-          a1[q][2 * cf] = p.x;
-          a1[q][2 * cf + 1] = p.y;
-        }
-#endif
+      for (int q = 0; q < 2; ++q) load_cache(a1[q], as(NF - 2) + q * kPad);
     }
     level<0, 0>(Sroot, 0);
   }
-
-  // sum over this lane's complete leaf rows of F(tau^-1 sum_c g), fixed order (kRegAcc only)
-  __device__ __forceinline__ double fsum_regs(double pad) const {
-    double part = 0.0;
-    if (c.t < c.beff) {
-#pragma unroll
-      for (int i = 0; i < (kRegAcc ? NBAT * RW : 1); ++i) part += f_of_mean(a, (racc[i] - pad) / a.tau);
-    }
-    return part;
-  }
 };
 
-template <int NF, int B, int G, bool STY>
-__global__ void __launch_bounds__(kFineThreads, 1) k_fine_tree(const FineArgs a) {
-  using T = Tree<NF, B>;
+template <int NF, int B, int G, bool STY, int NFR>
+__global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(const FineArgs a) {
+  using T = Tree<NF, B, NFR>;
+  using Run = TreeRun<NF, B, G, STY, NFR>;
+  constexpr int NT = T::THREADS, NW = T::WARPS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  FineCtx c;
-  c.grp = warp >> 2;
+  TreeCtx c;
   c.wm = warp & 3;
+  c.ch = (warp >> 2) % T::CH;
+  c.grp = warp / (4 * T::CH);
   c.g = lane >> 2;
   c.tg = lane & 3;
   c.t = c.wm * 8 + c.g;
+  c.cw = c.ch * 8 * NFR;
   c.r0 = (int64_t)blockIdx.x * kBundle;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
 
   // X^red of the subtree -> smem [level][run][q][t]; lane = t, rows (run, q) strided over warps
   {
-    const int t = tid & (kBundle - 1);
+    const int t = lane;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
       const int K = T::K(i), nrow = T::runs(i) * K;
       const double* src = a.lv[i].X + (c.r0 + t) * (int64_t)K;
       double* dst = fsm + T::XS + i * T::XL + t;
-      for (int r = tid >> 5; r < nrow; r += 4 * (kFineThreads >> 5)) {
+      for (int r = warp; r < nrow; r += 4 * NW) {
         double v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int rr = r + u * (kFineThreads >> 5);
+          const int rr = r + u * NW;
           const int j = rr / K, q = rr - j * K;
           v[u] = (rr < nrow && t < c.beff) ? src[(int64_t)j * a.Mroot * K + q] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int rr = r + u * (kFineThreads >> 5);
+          const int rr = r + u * NW;
           if (rr < nrow) dst[rr * kPad] = v[u];
         }
       }
     }
   }
-  using Run = TreeRun<NF, B, G, STY>;
   if constexpr (G > 0 && !Run::kRegAcc)
-    for (int e = tid; e < T::LEAVES * kBundle; e += kFineThreads) fsm[T::ACC + e] = 0.0;
+    for (int e = tid; e < T::ACCN; e += NT) fsm[T::ACC + e] = 0.0;
 
   // column tile operands (cp.async, double buffer): A rows [0, J) x 32 columns and the root tile
   const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
   auto load_tile = [&](int buf, int c0) {
     double* as = fsm + buf * T::ABUF;
     if (a.a_vec) {
-      for (int e = tid; e < T::J * (kFineBN / 2); e += kFineThreads) {
+      for (int e = tid; e < T::J * (kFineBN / 2); e += NT) {
         const int q = e >> 4, cc = (e & 15) * 2;
         const bool ok = c0 + cc < a.tau;
         cp_async16(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     } else {
-      for (int e = tid; e < T::J * kFineBN; e += kFineThreads) {
+      for (int e = tid; e < T::J * kFineBN; e += NT) {
         const int q = e >> 5, cc = e & 31;
         const bool ok = c0 + cc < a.tau;
         cp_async8(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     }
     double* rs = fsm + T::ROOT + buf * (kBundle * kPad);
-    for (int e = tid; e < kBundle * (kFineBN / 2); e += kFineThreads) {
+    for (int e = tid; e < kBundle * (kFineBN / 2); e += NT) {
       const int t = e >> 4, cc = (e & 15) * 2;
       const bool row_ok = a.root != nullptr && t < c.beff;
       const double* src = a.root + (c.r0 + t) * a.ldroot + c0 + cc;
@@ -397,16 +435,8 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine_tree(const FineArgs a)
       cp_async_wait<0>();
     }
     __syncthreads();
-    double Sroot[8];
-    {
-      const double* rs = fsm + T::ROOT + (ct & 1) * (kBundle * kPad) + c.t * kPad + 2 * c.tg;
-#pragma unroll
-      for (int cf = 0; cf < 4; ++cf) {
-        const double2 p = *reinterpret_cast<const double2*>(rs + cf * 8);
-        Sroot[2 * cf] = p.x;
-        Sroot[2 * cf + 1] = p.y;
-      }
-    }
+    double Sroot[T::NV];
+    run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (kBundle * kPad) + c.t * kPad);
     run.tile(Sroot);
     __syncthreads();
   }
@@ -416,22 +446,42 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine_tree(const FineArgs a)
     const double pad = (G == 2) ? (double)(ntiles * kFineBN - a.tau) : 0.0;
     double part = 0.0;
     if constexpr (Run::kRegAcc) {
-      part = run.fsum_regs(pad);
+      // column-slice partial row sums -> complete row sums: slices ch > 0 park theirs in smem (the
+      // X region is free after the last tile's barrier), slice 0 adds them in fixed order
+      constexpr int NA = Run::NACC;
+      double* park = fsm + T::XS + ((c.grp * 4 + c.wm) * 32 + lane) * NA;
+      if (c.ch > 0) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) park[(c.ch - 1) * (8 * 32 * NA) + i] = run.racc[i];
+      }
+      if constexpr (T::CH > 1) __syncthreads();
+      if (c.ch == 0 && c.t < c.beff) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+          double rs = run.racc[i];
+#pragma unroll
+          for (int h = 1; h < T::CH; ++h) rs += park[(h - 1) * (8 * 32 * NA) + i];
+          part += f_of_mean(a, (rs - pad) / a.tau);
+        }
+      }
     } else {
-      for (int e = tid; e < T::LEAVES * kBundle; e += kFineThreads) {
+      for (int e = tid; e < T::LEAVES * kBundle; e += NT) {
         const int t = e % kBundle;
         if (t >= c.beff) continue;
-        part += f_of_mean(a, (fsm[T::ACC + e] - pad) / a.tau);
+        double rs = fsm[T::ACC + e];
+#pragma unroll
+        for (int h = 1; h < T::CH; ++h) rs += fsm[T::ACC + h * (T::LEAVES * kBundle) + e];
+        part += f_of_mean(a, (rs - pad) / a.tau);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    __shared__ double red[kFineThreads / 32];
+    __shared__ double red[NW];
     if (lane == 0) red[warp] = part;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = 0; w < kFineThreads / 32; ++w) t += red[w];
+      for (int w = 0; w < NW; ++w) t += red[w];
       a.partial[blockIdx.x] = t;
     }
   }
@@ -439,23 +489,26 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine_tree(const FineArgs a)
 
 template <int NF, int B, int G, bool STY>
 static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_fine_tree<NF, B, G, STY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Tree<NF, B>::SMEM);
+  constexpr int NFR = RQMC_TREE_NFR;
+  using T = Tree<NF, B, NFR>;
+  if constexpr (T::SMEM > 227 * 1024) {
+    return cudaErrorNotSupported;
+  }
+  cudaError_t e = cudaFuncSetAttribute(k_fine_tree<NF, B, G, STY, NFR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       T::SMEM);
   if (e != cudaSuccess) return e;
-  k_fine_tree<NF, B, G, STY><<<(unsigned)nb, kFineThreads, Tree<NF, B>::SMEM, st>>>(a);
+  k_fine_tree<NF, B, G, STY, NFR><<<(unsigned)nb, T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
-// Does the fine level table have the compile-time shape Tree<NF, B> (and the same smem layout)?
+// Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
 template <int NF, int B>
 static bool tree_matches(const FineArgs& a) {
-  using T = Tree<NF, B>;
-  if (a.NF != NF || a.smem_bytes != T::SMEM || a.acc_off != T::ACC || a.leafruns != T::LEAVES) return false;
+  using T = Tree<NF, B, RQMC_TREE_NFR>;
+  if (a.NF != NF) return false;
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
-    if (L.K != T::K(i) || L.fan != B || L.runs != T::runs(i) || L.j_lo != T::jlo(i) || L.ldx != L.K ||
-        L.xs_off != T::XS + i * T::XL)
-      return false;
+    if (L.K != T::K(i) || L.fan != B || L.runs != T::runs(i) || L.j_lo != T::jlo(i) || L.ldx != L.K) return false;
   }
   return true;
 }
