@@ -1,8 +1,10 @@
-// a3+a4 coarse level GEMM (k_level_gemm); PAPER.md P:n.
+// a3+a4 coarse level GEMM (k_level_gemm): one level of paper Alg. 2,
+// R_w = tile(R_w') + X^red_w A_w, as a DMMA.8x8x4 (fp64 tensor core) GEMM.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -11,18 +13,42 @@
 namespace rqmc {
 
 // ------------------------------------------------------------------------------------------
-// a3+a4: coarse level GEMM  R[r, c] = Rp[r mod Mp, c] + sum_q X[r, q] A[q, c]
-// CTA tile BM x 64, K step 16, warps (BM/32) x 2 each 32 x 32 (4 x 4 DMMA fragments).
+// R[r, c] = Rp[r mod Mp, c] + sum_q X[r, q] A[q, c]   (the accumulator starts from the parent row)
+//
+// CTA tile BM x 64, k-tile 16, NST-stage cp.async ring (one barrier per k-tile; 2 stages measured
+// best: 3 equal, 4 slower), warps (BM/32) x 2
+// each 32 x 32 = 4 x 4 DMMA fragments (8 fragment loads per 16 DMMAs).
+// Row blocks are ordered sibling-first: CTA y = pb * nu + u covers rows u Mp + pb BM + [0, BM), so the
+// nu = M / Mp child blocks of one parent block run back to back and all but the first read the
+// parent tile from L2 (the parent R is read from HBM once instead of nu times).
 // ------------------------------------------------------------------------------------------
+#ifndef RQMC_GEMM_STAGES
+#define RQMC_GEMM_STAGES 2
+#endif
+#ifndef RQMC_GEMM_SIBLING
+#define RQMC_GEMM_SIBLING 1
+#endif
+constexpr int kGemmBN = 64, kGemmBK = 16, kGemmStages = RQMC_GEMM_STAGES;
+
+template <int BM>
+constexpr int gemm_smem_bytes() {
+  return (int)sizeof(double) * kGemmStages * (BM * (kGemmBK + 4) + kGemmBK * (kGemmBN + 4));
+}
+
 template <int BM, int CH>
-__global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
-  constexpr int BN = 64, BK = 16, XS = BK + 4, AS = BN + 4, NT = BM * 2;
+__global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu, int64_t y0) {
+  constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4, NT = BM * 2;
   extern __shared__ __align__(16) double gsm[];
   double (*Xs)[BM][XS] = reinterpret_cast<double (*)[BM][XS]>(gsm);
-  double (*As)[BK][AS] = reinterpret_cast<double (*)[BK][AS]>(gsm + 2 * BM * XS);
+  double (*As)[BK][AS] = reinterpret_cast<double (*)[BK][AS]>(gsm + NST * BM * XS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, tg = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.y * BM;
+  // sibling-first row blocks: rows [rb, rb + BM) of slice u, valid while inside the slice and < M
+  const int64_t yb = y0 + blockIdx.y;  // grid.y <= 65535: long levels launch in chunks
+  const int64_t pb = yb / nu, u = yb - pb * nu;
+  const int64_t in0 = pb * BM;                       // offset inside the slice
+  const int64_t r0 = u * mp_blk + in0;               // first row of the tile
+  const int64_t rlim = min(a.M, u * mp_blk + mp_blk);  // rows >= rlim belong to another tile
   const int c0 = blockIdx.x * BN;
 
   auto load_stage = [&](int buf, int k0) {
@@ -30,7 +56,7 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
     for (int c = tid; c < BM * (BK / 2); c += NT) {
       const int row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
       const int64_t gr = r0 + row;
-      const bool ok = gr < a.M && (k0 + kc) < a.ldx;
+      const bool ok = gr < rlim && (k0 + kc) < a.ldx;
       const double* src = ok ? a.X + gr * a.ldx + k0 + kc : a.X;
       cp_async16(&Xs[buf][row][kc], src, ok);
     }
@@ -42,11 +68,14 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
       if (CH == 2) cp_async16(&As[buf][row][cc], src, ok);
       else cp_async8(&As[buf][row][cc], src, ok);
     }
-    cp_async_commit();
   };
 
   const int nk = (a.K + BK - 1) / BK;
-  load_stage(0, 0);
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) {
+    if (s < nk) load_stage(s, s * BK);
+    cp_async_commit();
+  }
 
   double acc[4][4][2];
 #pragma unroll
@@ -57,23 +86,26 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
       acc[i][jn][0] = 0.0;
       acc[i][jn][1] = 0.0;
-      if (a.Rp && row < a.M) {  // tile(R_w'): row r reads parent row r mod M_w'
+      if (a.Rp && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
         const double* p = a.Rp + (row % a.Mp) * a.ldp + col;
-        if (col < a.tau) acc[i][jn][0] = p[0];
-        if (col + 1 < a.tau) acc[i][jn][1] = p[1];
+        if (CH == 2 && col + 1 < a.tau) {
+          const double2 v = *reinterpret_cast<const double2*>(p);
+          acc[i][jn][0] = v.x;
+          acc[i][jn][1] = v.y;
+        } else {
+          if (col < a.tau) acc[i][jn][0] = p[0];
+          if (col + 1 < a.tau) acc[i][jn][1] = p[1];
+        }
       }
     }
   }
 
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) {
-      load_stage(buf ^ 1, (kt + 1) * BK);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    cp_async_wait<NST - 2>();
+    __syncthreads();  // stage kt landed for all threads; stage kt-1's buffer is free
+    if (kt + NST - 1 < nk) load_stage((kt + NST - 1) % NST, (kt + NST - 1) * BK);
+    cp_async_commit();
+    const int buf = kt % NST;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[4], bf[4];
@@ -86,13 +118,13 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t row = r0 + wm * 32 + i * 8 + g;
-    if (row >= a.M) continue;
+    if (row >= rlim) continue;
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
@@ -107,14 +139,26 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a) {
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
-  const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0);
+  if (a.M == 0) return cudaSuccess;
+  const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
+                   (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
   const int BM = a.M >= 64 * 148 ? 128 : 64;
-  dim3 grid((unsigned)((a.tau + 63) / 64), (unsigned)((a.M + BM - 1) / BM));
-  const int sm = (int)sizeof(double) * 2 * (BM * 20 + 16 * 68);
+  // sibling-first ordering when the parent has at least one full row block; else plain row blocks
+  int64_t mp_blk = a.M, nu = 1;
+  if (RQMC_GEMM_SIBLING && a.Rp && a.Mp >= BM && a.Mp < a.M) {
+    mp_blk = a.Mp;
+    nu = (a.M + a.Mp - 1) / a.Mp;
+  }
+  const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
+  const int sm = BM == 128 ? gemm_smem_bytes<128>() : gemm_smem_bytes<64>();
   auto go = [&](auto kern, int nt) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    kern<<<grid, nt, sm, st>>>(a);
+    // grid.x = column blocks (fastest: the 32 CTAs of one row block share its X^red rows in L2)
+    for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
+      dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0));
+      kern<<<grid, nt, sm, st>>>(a, mp_blk, nu, y0);
+    }
     return cudaGetLastError();
   };
   if (BM == 128) return vec ? go(k_level_gemm<128, 2>, 256) : go(k_level_gemm<128, 1>, 256);

@@ -364,37 +364,30 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
   c.r0 = (int64_t)blockIdx.x * kBundle;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
 
-  // X^red of the subtree -> smem [level][run][q][t]; lane = t, rows (run, q) strided over warps
-  {
-    const int t = lane;
+  // X^red of the subtree -> smem [level][run][q][t]: the bundle's rows of one run are 32 K contiguous
+  // doubles in HBM, read coalesced by 8-byte cp.async and transposed on the way into smem
 #pragma unroll
-    for (int i = 0; i < NF; ++i) {
-      const int K = T::K(i), nrow = T::runs(i) * K;
-      const double* src = a.lv[i].X + (c.r0 + t) * (int64_t)K;
-      double* dst = fsm + T::XS + i * T::XL + t;
-      for (int r = warp; r < nrow; r += 4 * NW) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int rr = r + u * NW;
-          const int j = rr / K, q = rr - j * K;
-          v[u] = (rr < nrow && t < c.beff) ? src[(int64_t)j * a.Mroot * K + q] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int rr = r + u * NW;
-          if (rr < nrow) dst[rr * kPad] = v[u];
-        }
-      }
+  for (int i = 0; i < NF; ++i) {
+    const int K = T::K(i), n = T::runs(i) * kBundle * K;
+    const double* src = a.lv[i].X + c.r0 * (int64_t)K;
+    double* dst = fsm + T::XS + i * T::XL;
+    for (int e = tid; e < n; e += NT) {
+      const int j = e / (kBundle * K), r = e - j * (kBundle * K), t = r / K, q = r - t * K;
+      const bool ok = t < c.beff;
+      cp_async8(dst + (j * K + q) * kPad + t, ok ? src + (int64_t)j * a.Mroot * K + r : a.A, ok);
     }
   }
+  cp_async_commit();
   if constexpr (G > 0 && !Run::kRegAcc)
     for (int e = tid; e < T::ACCN; e += NT) fsm[T::ACC + e] = 0.0;
 
-  // column tile operands (cp.async, double buffer): A rows [0, J) x 32 columns and the root tile
+  // column tile operands (cp.async, double buffer): A rows [0, J) x 32 columns and the root tile.
+  // (One 256-byte cp.async.bulk per row completing on an mbarrier measured 2.1 ms slower on C5: the
+  // 95 small bulk requests per tile serialise in the copy engine.)
   const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
   auto load_tile = [&](int buf, int c0) {
     double* as = fsm + buf * T::ABUF;
+    double* rs = fsm + T::ROOT + buf * (kBundle * kPad);
     if (a.a_vec) {
       for (int e = tid; e < T::J * (kFineBN / 2); e += NT) {
         const int q = e >> 4, cc = (e & 15) * 2;
@@ -408,7 +401,6 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
         cp_async8(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     }
-    double* rs = fsm + T::ROOT + buf * (kBundle * kPad);
     for (int e = tid; e < kBundle * (kFineBN / 2); e += NT) {
       const int t = e >> 4, cc = (e & 15) * 2;
       const bool row_ok = a.root != nullptr && t < c.beff;
@@ -425,20 +417,17 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
 
   Run run(a, c);
   load_tile(0, 0);
+  cp_async_wait<0>();  // X^red subtree and tile 0 resident
+  __syncthreads();
   for (int ct = 0; ct < ntiles; ++ct) {
     c.c0 = ct * kFineBN;
     c.as = fsm + (ct & 1) * T::ABUF;
-    if (ct + 1 < ntiles) {
-      load_tile((ct + 1) & 1, (ct + 1) * kFineBN);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    if (ct + 1 < ntiles) load_tile((ct + 1) & 1, (ct + 1) * kFineBN);  // buffer freed by the last barrier
     double Sroot[T::NV];
     run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (kBundle * kPad) + c.t * kPad);
     run.tile(Sroot);
-    __syncthreads();
+    cp_async_wait<0>();
+    __syncthreads();  // tile ct + 1 landed and visible; buffers (ct & 1) free for tile ct + 2
   }
 
   if constexpr (G > 0) {
