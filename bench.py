@@ -188,8 +188,15 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    Y = None
+    if prob.store_y:   # configs whose output is the full XA (C1, C4): Y written to HBM every step
+        Y = torch.empty((prob.N // world, prob.tau), dtype=torch.float64, device="cuda")
+
     def step():
-        plan.qn_sum(A, prob.f, prob.fparam, out=fsum)
+        if Y is not None:
+            plan.xa(A, prob.f, prob.fparam, Y=Y, fsum=fsum)
+        else:
+            plan.qn_sum(A, prob.f, prob.fparam, out=fsum)
         if world > 1:
             dist.all_reduce(fsum)
 
@@ -229,15 +236,24 @@ def main():
     # ---- end-to-end through the public API with host buffers (pinned A in, f-sum out)
     A_pin = torch.from_numpy(prob.A.copy()).pin_memory()
     A_host = A_pin.numpy()
+    A_e2e = torch.empty_like(A)
+
+    def e2e_call():
+        if Y is None:   # C ABI rqmc_qn_host: H2D of A and D2H of the f-sum inside the call
+            return plan.qn_host(A_host, prob.f, prob.fparam)
+        A_e2e.copy_(A_pin, non_blocking=True)   # XA configs: Y stays a device-resident output
+        plan.xa(A_e2e, prob.f, prob.fparam, Y=Y, fsum=fsum)
+        return float(fsum.item())
+
     for _ in range(2):
-        plan.qn_host(A_host, prob.f, prob.fparam)
+        e2e_call()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e2e_ms = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        part = plan.qn_host(A_host, prob.f, prob.fparam)
+        part = e2e_call()
         if world > 1:
             pt = torch.tensor([part], dtype=torch.float64, device="cuda")
             dist.all_reduce(pt)
@@ -264,14 +280,38 @@ def main():
         except Exception:
             traffic = None
     dominant = "k_fine" if prof["fine_ms"] >= prof["coarse_ms"] else "k_level_gemm"
-    if dominant == "k_fine":
+    peak = FP64_PEAK_DERIVED / 1e12
+    unit, peak_note = "TFLOP/s", ("fp64 148 SM x 128 flop/clk x 1.965 GHz (derived, DESIGN.md); "
+                                  "probe measured DFMA 36.8, DMMA 37.0 TF/s (profiles/r01_fp64_probe.jsonl)")
+    algo = fine_flops if dominant == "k_fine" else coarse_flops
+    if dominant == "k_fine" and Y is not None:
+        # XA stored: the fused fine kernel streams Y (8 N tau bytes) to HBM -- the bound
+        algo = 8.0 * (prob.N // world) * prob.tau
+        ach, bound, unit = algo / (fine_ms * 1e-3) / 1e9, "hbm", "GB/s"
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+        peak_note = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    elif dominant == "k_fine":
         ach = fine_flops / (fine_ms * 1e-3) / 1e12
         bound = "alu"
     else:
         ach = coarse_flops / (coarse_ms * 1e-3) / 1e12
         bound = "tensor"
-    peak = FP64_PEAK_DERIVED / 1e12
     total_flops = 2.0 * plan.stats()["macs"]
+
+    # whole-step roofline: t_roof = max(F / P64, B / BW), F = 2 tau sum_w M_w s_w,
+    # B = 8 s tau (A read once) + 8 N tau when Y is stored
+    p64 = FP64_PEAK_DERIVED
+    bw = 1e9 * (json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0)
+    t_step = ms_max / args.steps * 1e-3
+    f_step = total_flops / world
+    b_step = 8.0 * prob.s * prob.tau + (8.0 * (prob.N // world) * prob.tau if Y is not None else 0.0)
+    t_roof = max(f_step / p64, b_step / bw)
+    step_roof = {"flops_per_step": f_step, "bytes_per_step": b_step,
+                 "bound": "fp64" if f_step / p64 >= b_step / bw else "hbm",
+                 "t_roof_ms": t_roof * 1e3, "achieved_tflops": f_step / t_step / 1e12,
+                 "achieved_gbs": b_step / t_step / 1e9, "frac": t_roof / t_step}
 
     n_coarse = ck + 1
     launches_per_step = 1 + n_coarse + 1 + 1   # k_gen + coarse GEMMs + k_fine + k_reduce
@@ -292,18 +332,15 @@ def main():
                    "parallelism": f"residue classes k mod {world}" if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write, outside the step events)",
                    "checkpoint_w": levels[ck]["w"], "fused_fine_levels": summ["n_fine"]},
-        "roofline": {"kernel": dominant, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                     "frac": ach / peak, "traffic": traffic,
-                     "peak_note": "fp64 148 SM x 128 flop/clk x 1.965 GHz (derived, DESIGN.md); "
-                                  "probe measured DFMA 36.8, DMMA 37.0 TF/s (profiles/r01_fp64_probe.jsonl)",
-                     "algorithmic_flops_per_launch": fine_flops if dominant == "k_fine" else coarse_flops},
-        "step_roofline": {"flops_per_step": total_flops / world,
-                          "achieved_tflops": total_flops / world / (ms_max / args.steps * 1e-3) / 1e12,
-                          "frac": total_flops / world / (ms_max / args.steps * 1e-3) / 1e12 / peak},
+        "roofline": {"kernel": dominant, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                     "frac": ach / peak, "traffic": traffic, "peak_note": peak_note,
+                     ("algorithmic_bytes_per_launch" if unit == "GB/s" else "algorithmic_flops_per_launch"): algo},
+        "step_roofline": step_roof,
         "phases_ms_per_step": {k: v / runs for k, v in prof.items() if k.endswith("_ms")},
         "e2e": {"value": prob.N * prob.tau / (e2e_tot / args.steps * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(prob.s * prob.tau * 8), "d2h_bytes_per_step": 8,
-                "api": "rqmc_qn_host (pinned host A -> device, local f-sum -> host)"},
+                "api": "rqmc_qn_host (pinned host A -> device, local f-sum -> host)" if Y is None else
+                       "Plan.xa (pinned host A -> device copy, Y device-resident output, f-sum -> host)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "qn": qn_val,

@@ -4,9 +4,33 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <vector>
+
 #include "rqmc_internal.h"
 
 namespace rqmc {
+
+// cudaFuncSetAttribute(max dynamic smem) once per kernel, device and size (a driver call per launch
+// costs microseconds: visible on the small configs C1/C2)
+struct SmemAttr { const void* fn; int dev; int bytes; };
+inline cudaError_t set_smem_once_raw(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<SmemAttr> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const SmemAttr& d : done)
+    if (d.fn == fn && d.dev == dev && d.bytes >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({fn, dev, bytes});
+  return e;
+}
+template <class F>
+inline cudaError_t set_smem_once(F* kern, int bytes) {
+  return set_smem_once_raw(reinterpret_cast<const void*>(kern), bytes);
+}
 
 // ------------------------------------------------------------------------------------------
 // async copy helpers

@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
 
 template <int NF, class BT>
 static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(k_fine<NF, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+  cudaError_t e = set_smem_once(k_fine<NF, BT>, a.smem_bytes);
   if (e != cudaSuccess) return e;
   k_fine<NF, BT><<<(unsigned)nb, kFineThreads, a.smem_bytes, st>>>(a);
   return cudaGetLastError();

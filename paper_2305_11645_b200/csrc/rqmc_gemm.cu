@@ -152,7 +152,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
   const int sm = BM == 128 ? gemm_smem_bytes<128>() : gemm_smem_bytes<64>();
   auto go = [&](auto kern, int nt) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaError_t e = set_smem_once(kern, sm);
     if (e != cudaSuccess) return e;
     // grid.x = column blocks (fastest: the 32 CTAs of one row block share its X^red rows in L2)
     for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {

@@ -483,8 +483,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, cudaStream_t st)
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
   }
-  cudaError_t e = cudaFuncSetAttribute(k_fine_tree<NF, B, G, STY, NFR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       T::SMEM);
+  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR>, T::SMEM);
   if (e != cudaSuccess) return e;
   k_fine_tree<NF, B, G, STY, NFR><<<(unsigned)nb, T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
