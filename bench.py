@@ -36,7 +36,7 @@ FP64_PEAK_DERIVED = 148 * 128 * 1.965e9      # SMs x fp64 flop/clk/SM x max SM c
 
 
 def describe(prob) -> str:
-    kind = "lattice" if prob.kind == W.KIND_LATTICE else "digital net"
+    kind = {W.KIND_LATTICE: "lattice", W.KIND_NET: "digital net", W.KIND_MC: "reduced MC"}[prob.kind]
     sh = "shift" if (prob.shift is not None or prob.dshift is not None) else "no shift"
     mp = "Phi^-1" if prob.map == W.MAP_INVNORM else "unit cube"
     fn = {0: "exp(mean)", 1: "max(mean(exp(0.2y))-1,0)", 2: "mean(y^2)", 3: "mean(y)"}[prob.f]

@@ -25,6 +25,7 @@
  *  - Layouts: A row-major s x tau, row j = a_j, leading dimension lda >= tau (elements).
  *    Y row-major (N/world) x tau, ldy >= tau; local row i is global point k = rank + world * i
  *    (residue-class partition, multi-GPU; world = 1 gives Y = XA).
+ *  - Point kinds: RQMC_LATTICE, RQMC_DIGITAL_NET (b = 2) and RQMC_REDUCED_MC (see rqmc_kind).
  *  - Precision: fp64 throughout.  Point indices/digits are exact integers; lattice values are
  *    u = t/M (IEEE divide), shift u = u + Delta, if u >= 1 then u - 1 (no FMA contraction).
  *  - Limits: N = b^m <= 2^32; m <= 53 for nets; world must be a power of b dividing N.
@@ -56,7 +57,17 @@ typedef enum {
   RQMC_EUNSUPPORTED = 11 /* outside the supported envelope (N > 2^32, world, ...)          */
 } rqmc_status;
 
-typedef enum { RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1 } rqmc_kind;
+/* RQMC_REDUCED_MC: reduced Monte Carlo (Sec. 5, Eq. randpts): coordinate j
+ * draws only N_j = b^{m - min(w_j,m)} i.i.d. uniforms y_{j,0..N_j-1} and point n uses
+ * x_{n,j} = y_{j, n mod N_j} (the truncated mixed-radix index of Eq. randpts equals n mod N_j).
+ * The draws come from a counter-based generator (both the product path and the test oracle
+ * implement it):  mix64(x) = SplitMix64 finaliser (x ^= x>>30; x *= 0xBF58476D1CE4E5B9;
+ * x ^= x>>27; x *= 0x94D049BB133111EB; x ^= x>>31), G = 0x9E3779B97F4A7C15,
+ *   key_j = mix64(seed * G + (j+1))      (j 0-based coordinate, wrapping uint64 arithmetic)
+ *   word  = mix64(key_j + (r+1) * G) >> 11,  u = (word | 1) 2^-53   (exact, odd multiple of
+ *   2^-53, so 0 < u < 1 and Phi^-1(u) is finite).
+ * The same tree of levels, GEMMs and fused fine kernel computes the product. */
+typedef enum { RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1, RQMC_REDUCED_MC = 2 } rqmc_kind;
 typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1 } rqmc_map;
 
 /* f(y) = F(tau^-1 sum_c g(y_c))  (SURVEY reading C-17)                                    */
@@ -83,6 +94,7 @@ typedef struct {
   const uint64_t* dshift;   /* net digital shift sigma_j < 2^53: x = ((W << (53-m)) ^ sigma) 2^-53 */
   rqmc_map map;             /* RQMC_MAP_INVNORM: x = Phi^-1(u), u = 0 remapped (reading C-5) */
   int rank, world;          /* residue-class partition k = rank (mod world); (0,1) = whole   */
+  uint64_t seed;            /* RQMC_REDUCED_MC: generator seed (z, C, shift, dshift unused)  */
 } rqmc_plan_desc;
 
 /* Level table entry (coarse -> fine), for inspection and tests. */

@@ -5,7 +5,8 @@ The product path (paper_2305_11645_b200) never imports it and shares no code wit
 
 Thin ctypes wrapper over oracle/rqmc_oracle.c (plain C, fp64, -ffp-contract=off), which computes
 the plain definitions of PAPER.md (P:n = line n):
-  points  x_{k,j} = {k z_j / N} + shift / digital net + Phi^-1 map
+  points  x_{k,j} = {k z_j / N} + shift / digital net / reduced MC
+          (Eq. randpts) + Phi^-1 map
   product Y = X A, naive triple loop in increasing j
   Q_N     N^-1 sum_k f(x_k^T A) with Neumaier summation
 Every function is pinned by tests/test_oracle_pins.py.
@@ -37,7 +38,7 @@ class _Prob(C.Structure):
                 ("w", C.POINTER(C.c_int32)), ("kind", C.c_int),
                 ("z", C.POINTER(C.c_uint64)), ("C", C.POINTER(C.c_uint64)),
                 ("shift", C.POINTER(C.c_double)), ("dshift", C.POINTER(C.c_uint64)),
-                ("map", C.c_int)]
+                ("map", C.c_int), ("seed", C.c_uint64)]
 
 
 _lib = None
@@ -59,6 +60,11 @@ def lib():
         _lib.orc_f_rows_meanid.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, i64p, C.c_int64, dp, C.c_int]
         _lib.orc_points_rows.argtypes = [C.POINTER(_Prob), i64p, C.c_int64, dp, C.c_int]
         _lib.orc_f_all_meanid_tab.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, C.c_int]
+        _lib.orc_mc_bank_index.restype = C.c_uint64
+        _lib.orc_mc_bank_index.argtypes = [C.POINTER(_Prob), C.c_uint64, C.c_int]
+        _lib.orc_mc_word.restype = C.c_uint64
+        _lib.orc_mc_word.argtypes = [C.c_uint64, C.c_int, C.c_uint64]
+        _lib.orc_mc_points_bank.argtypes = [C.POINTER(_Prob), dp, i64p, C.c_int64, C.c_int64, dp]
     return _lib
 
 
@@ -77,7 +83,31 @@ class _Holder:
         self.ds = None if prob.dshift is None else np.ascontiguousarray(prob.dshift, dtype=np.uint64)
         self.s = _Prob(prob.b, prob.m, prob.s, _ptr(self.w, C.c_int32), prob.kind,
                        _ptr(self.z, C.c_uint64), _ptr(self.Cm, C.c_uint64),
-                       _ptr(self.sh, C.c_double), _ptr(self.ds, C.c_uint64), prob.map)
+                       _ptr(self.sh, C.c_double), _ptr(self.ds, C.c_uint64), prob.map,
+                       int(getattr(prob, "mc_seed", 0)))
+
+
+def mc_bank_index(prob, n: int, j: int) -> int:
+    """Reduced MC (Eq. randpts): bank sample number used by coordinate j (0-based) of point n."""
+    h = _Holder(prob)
+    return int(lib().orc_mc_bank_index(C.byref(h.s), n, j))
+
+
+def mc_word(seed: int, j: int, r: int) -> int:
+    """The counter-based draw y_{j,r} as its 53-bit word (u = (word | 1) 2^-53)."""
+    return int(lib().orc_mc_word(seed, j, r))
+
+
+def mc_points_bank(prob, bank_cols, k0: int = 0, n: int | None = None) -> np.ndarray:
+    """Sample matrix of Eq. randpts from explicit banks: bank_cols[j] holds N_j values of coordinate j."""
+    n = prob.N - k0 if n is None else n
+    h = _Holder(prob)
+    off = np.zeros(prob.s, dtype=np.int64)
+    off[1:] = np.cumsum([len(c) for c in bank_cols])[:-1]
+    bank = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64) for c in bank_cols]))
+    X = np.empty((n, prob.s), dtype=np.float64)
+    lib().orc_mc_points_bank(C.byref(h.s), _ptr(bank, C.c_double), _ptr(off, C.c_int64), k0, n, _ptr(X, C.c_double))
+    return X
 
 
 def invnorm(u: float) -> float:

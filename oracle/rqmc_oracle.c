@@ -14,6 +14,8 @@
  *        net      vec y_{j,n} = Chat^(j) vec n, y = vec y . (b^-1..b^-m)    (Eq. def:digital)
  *                 Chat^(j): last min(w_j,m) rows of C^(j) set to zero      (Eq. reduced_genmat_net2)
  *        digital shift (reading C-9): V = (W << (53-m)) XOR sigma_j, x = V 2^-53
+ *        reduced MC (Eq. randpts) x_{j,n} = y_{j, m_s N_{s+1} + ... + m_j N_{j+1}} from the
+ *                 mixed-radix digits of n; the bank y_{j,r} is the counter-based stream of include/rqmc.h
  *        map      x = Phi^-1(u), zero rule reading C-5
  *   O2 product Y[k,c] = sum_{j=1..s} x_{k,j} A[j,c], increasing j
  *   O3 f_k = F(tau^-1 sum_c g(Y[k,c])) (increasing c); sum_k f_k Neumaier-compensated
@@ -39,6 +41,7 @@ typedef struct {
   const double* shift;     /* lattice Delta_j in [0,1) or NULL */
   const uint64_t* dshift;  /* net sigma_j < 2^53 or NULL */
   int map;                 /* 0 identity, 1 Phi^-1 */
+  uint64_t seed;           /* kind 2 (reduced Monte Carlo): seed of the counter-based draws */
 } orc_problem;
 
 static uint64_t ipow(uint64_t b, int e) {
@@ -77,6 +80,48 @@ static double orc_map(const orc_problem* p, double u, int shifted) {
   return orc_invnorm(u);
 }
 
+/* ---- reduced Monte Carlo (Sec. 5) ------------------------------------------------- */
+
+/* Eq. randpts: with N_j = b^{m - w_j} (w_j clamped to m), N_{s+1} = 1, M_j = N_j / N_{j+1}, write
+ * n = m_s N_{s+1} + m_{s-1} N_s + ... + m_1 N_2 with 0 <= m_i < M_i; coordinate j of
+ * point n takes bank sample number m_s N_{s+1} + ... + m_j N_{j+1} (digits j..s only). */
+uint64_t orc_mc_bank_index(const orc_problem* p, uint64_t n, int j) {
+  uint64_t idx = 0, rem = n;
+  for (int i = p->s - 1; i >= 0; --i) {                     /* i = s-1 .. 0 <-> paper's s .. 1 */
+    const int wi = p->w[i] < p->m ? p->w[i] : p->m;
+    const int wn = (i + 1 < p->s) ? (p->w[i + 1] < p->m ? p->w[i + 1] : p->m) : p->m;  /* w_{s+1} = m */
+    const uint64_t Ni1 = ipow((uint64_t)p->b, p->m - wn);  /* N_{i+1} */
+    const uint64_t Mi = ipow((uint64_t)p->b, wn - wi);     /* M_i = N_i / N_{i+1} */
+    const uint64_t mi = rem % Mi;                          /* digit m_i (radix M_i, weight N_{i+1}) */
+    rem /= Mi;
+    if (i >= j) idx += mi * Ni1;
+  }
+  return idx;
+}
+
+/* the counter-based draw y_{j,r} (include/rqmc.h, rqmc_kind): 53-bit word and u = (word|1) 2^-53 */
+static uint64_t orc_mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+uint64_t orc_mc_word(uint64_t seed, int j, uint64_t r) {
+  const uint64_t G = 0x9E3779B97F4A7C15ull;
+  const uint64_t key = orc_mix64(seed * G + (uint64_t)(j + 1));
+  return orc_mix64(key + (r + 1) * G) >> 11;
+}
+
+/* Eq. randpts with an explicit bank: X[i][j] = bank[off[j] + index_j(k0 + i)] (the sample matrix of
+ * SPEC's reduced-MC module; used with finite discrete banks by the exact-variance pin). */
+int orc_mc_points_bank(const orc_problem* p, const double* bank, const int64_t* off, int64_t k0,
+                       int64_t n, double* X) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < p->s; ++j)
+      X[i * p->s + j] = bank[off[j] + (int64_t)orc_mc_bank_index(p, (uint64_t)(k0 + i), j)];
+  return 0;
+}
+
 /* O1 for one entry: coordinate j of point k (value, and its integer word in *word). */
 double orc_point(const orc_problem* p, uint64_t k, int j, uint64_t* word_out) {
   const uint64_t N = ipow((uint64_t)p->b, p->m);
@@ -84,6 +129,12 @@ double orc_point(const orc_problem* p, uint64_t k, int j, uint64_t* word_out) {
   double u;
   uint64_t word;
   int shifted;
+  if (p->kind == 2) {
+    word = orc_mc_word(p->seed, j, orc_mc_bank_index(p, k, j));
+    if (word_out) *word_out = word;
+    u = (double)(word | 1u) * ldexp(1.0, -53);              /* in (0,1): no zero rule needed */
+    return p->map == 0 ? u : orc_invnorm(u);
+  }
   if (p->kind == 0) {
     /* z_j = b^{w_j} z'_j; for w_j >= m, z_j is a multiple of N. */
     uint64_t zj = wj >= p->m ? 0 : (uint64_t)(((unsigned __int128)ipow((uint64_t)p->b, wj) * p->z[j]) % N);

@@ -24,7 +24,7 @@ from ._build import LIB as _LIB_PATH
 # A/B experiments only: RQMC_LIB may name another in-tree build (librqmc_<variant>.so)
 _LIB_PATH = os.environ.get("RQMC_LIB", _LIB_PATH)
 
-LATTICE, DIGITAL_NET = 0, 1
+LATTICE, DIGITAL_NET, REDUCED_MC = 0, 1, 2
 MAP_UNIT, MAP_INVNORM = 0, 1
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
 
@@ -44,7 +44,7 @@ class _Desc(C.Structure):
                 ("w", C.POINTER(C.c_int32)), ("kind", C.c_int),
                 ("z", C.POINTER(C.c_uint64)), ("C", C.POINTER(C.c_uint64)),
                 ("shift", C.POINTER(C.c_double)), ("dshift", C.POINTER(C.c_uint64)),
-                ("map", C.c_int), ("rank", C.c_int), ("world", C.c_int)]
+                ("map", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("seed", C.c_uint64)]
 
 
 class LevelInfo(C.Structure):
@@ -121,12 +121,12 @@ class Plan:
 
     def __init__(self, b: int, m: int, s: int, tau: int, w: Sequence[int], kind: int = LATTICE,
                  z=None, C_words=None, shift=None, dshift=None, map: int = MAP_UNIT,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, seed: int = 0):
         self._keep = dict(w=_arr(w, np.int32), z=_arr(z, np.uint64), C=_arr(C_words, np.uint64),
                           shift=_arr(shift, np.float64), dshift=_arr(dshift, np.uint64))
         k = self._keep
         d = _Desc(b, m, s, tau, _p(k["w"], C.c_int32), kind, _p(k["z"], C.c_uint64), _p(k["C"], C.c_uint64),
-                  _p(k["shift"], C.c_double), _p(k["dshift"], C.c_uint64), map, rank, world)
+                  _p(k["shift"], C.c_double), _p(k["dshift"], C.c_uint64), map, rank, world, seed)
         h = C.c_void_p()
         st = lib().rqmc_plan_create(C.byref(d), C.byref(h))
         if st != 0:
@@ -139,7 +139,7 @@ class Plan:
     @classmethod
     def from_problem(cls, prob, rank: int = 0, world: int = 1) -> "Plan":
         return cls(prob.b, prob.m, prob.s, prob.tau, prob.w, prob.kind, prob.z, prob.C, prob.shift,
-                   prob.dshift, prob.map, rank, world)
+                   prob.dshift, prob.map, rank, world, getattr(prob, "mc_seed", 0))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -30,6 +30,7 @@ struct GenArgs {
   const double* shift;           // lattice Delta_j
   const uint64_t* C;             // net column words (row-zeroed)
   const uint64_t* dshift;        // net sigma_j
+  uint64_t seed;                 // reduced MC generator seed
   double* X;                     // workspace base
   GenLevel lv[kMaxLevels];
 };

@@ -53,6 +53,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct rqmc_plan_s {
   int b = 0, m = 0, s = 0, tau = 0, kind = 0, map = 0, rank = 0, world = 1;
   bool shifted = false;
+  uint64_t seed = 0;         // reduced MC
   int64_t N = 0, Nl = 0;
   int s_star = 0;
   std::vector<int32_t> w;
@@ -153,7 +154,8 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   if (d->m < 1 || d->s < 1 || d->tau < 1) return bad(RQMC_EDIM, "m, s, tau must be >= 1");
   if (!is_prime(d->b)) return bad(RQMC_ENOTPRIME, "b = " + std::to_string(d->b) + " is not prime");
   if (!d->w) return bad(RQMC_EINVAL, "w is NULL");
-  if (d->kind != RQMC_LATTICE && d->kind != RQMC_DIGITAL_NET) return bad(RQMC_EINVAL, "bad kind");
+  if (d->kind != RQMC_LATTICE && d->kind != RQMC_DIGITAL_NET && d->kind != RQMC_REDUCED_MC)
+    return bad(RQMC_EINVAL, "bad kind");
   if (d->map != RQMC_MAP_UNIT && d->map != RQMC_MAP_INVNORM) return bad(RQMC_EINVAL, "bad map");
   if (d->m * std::log2((double)d->b) > 32.0 + 1e-9) return bad(RQMC_EUNSUPPORTED, "N = b^m > 2^32");
   if (d->kind == RQMC_DIGITAL_NET && (d->b != 2 || d->m > 32))
@@ -182,7 +184,11 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   for (int j = 0; j < d->s; ++j)
     if (d->w[j] < d->m) p->s_star = j + 1;
 
-  if (d->kind == RQMC_LATTICE) {
+  if (d->kind == RQMC_REDUCED_MC) {
+    // i.i.d. draws per coordinate: no generating vector, matrices or shifts
+    if (d->shift || d->dshift) { delete p; return bad(RQMC_ESHIFT, "reduced MC takes no shift (its draws are random)"); }
+    p->seed = d->seed;
+  } else if (d->kind == RQMC_LATTICE) {
     if (!d->z) { delete p; return bad(RQMC_EINVAL, "z is NULL"); }
     p->z.assign(d->z, d->z + d->s);
     for (int j = 0; j < d->s; ++j) {
@@ -247,7 +253,8 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       while (j2 < d->s && std::min<int>(d->w[j2], d->m) == wl) ++j2;
       // columns j > s* are x = 0: dropped, unless a shift or the map makes them the
       // constant phi_j(Delta_j) / Phi^-1(zero rule) -- then a 1-row level m (reading C-4)
-      if (wl < d->m || p->shifted || d->map != RQMC_MAP_UNIT) {
+      // (reduced MC: N_j = 1 for w_j >= m -- one i.i.d. draw per coordinate, P:981 N_{s+1} = 1)
+      if (wl < d->m || p->shifted || d->map != RQMC_MAP_UNIT || d->kind == RQMC_REDUCED_MC) {
         Level L{};
         L.w = wl; L.j_lo = j; L.s_w = j2 - j;
         L.M = ipow(d->b, d->m - wl);
@@ -390,6 +397,7 @@ GenArgs gen_args(const rqmc_plan_s* p, void* work) {
   g.kind = p->kind; g.map = p->map; g.b = p->b; g.m = p->m; g.shifted = p->shifted;
   g.rank = p->rank; g.world = p->world; g.nlev = (int)p->lv.size();
   g.zero_u = p->shifted ? std::ldexp(1.0, -53) : 0.5 / (double)p->N;
+  g.seed = p->seed;
   g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds;
   g.X = reinterpret_cast<double*>(static_cast<char*>(work) + p->off_x);
   for (size_t i = 0; i < p->lv.size(); ++i) {

@@ -160,7 +160,7 @@ def a_kl(s: int, tau: int) -> np.ndarray:
 
 # f ids (match include/rqmc.h rqmc_f)
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
-KIND_LATTICE, KIND_NET = 0, 1
+KIND_LATTICE, KIND_NET, KIND_MC = 0, 1, 2
 MAP_UNIT, MAP_INVNORM = 0, 1
 
 
@@ -184,15 +184,27 @@ class Problem:
     fparam: np.ndarray                 # float64[2]
     store_y: bool
     seed: int
+    mc_seed: int = 0                   # reduced MC (KIND_MC): seed of the counter-based draws
 
     @property
     def N(self) -> int:
         return self.b ** self.m
 
 
+def as_reduced_mc(prob: Problem, mc_seed: Optional[int] = None) -> Problem:
+    """The same layout (b, m, w), map, A and f with reduced Monte Carlo points (Sec. 5,
+    P:975-1000): no generating vector / matrices / shifts, draws seeded by
+    mc_seed (default: the problem's seed)."""
+    return dataclasses.replace(prob, name=prob.name + "MC", kind=KIND_MC, z=None, C=None, shift=None,
+                               dshift=None, mc_seed=int(prob.seed if mc_seed is None else mc_seed))
+
+
 def make_config(cfg: str, seed: Optional[int] = None) -> Problem:
-    """BASELINE.json configs C1..C5 (SURVEY §8(d) 'Inputs (exact)')."""
+    """BASELINE.json configs C1..C5 (SURVEY §8(d) 'Inputs (exact)'); a suffix "MC" (e.g. C5MC) gives
+    the same workload with reduced Monte Carlo points (as_reduced_mc)."""
     cfg = cfg.upper()
+    if cfg.endswith("MC"):
+        return as_reduced_mc(make_config(cfg[:-2], seed))
     seeds = {"C1": 1001, "C2": 1002, "C3": 1003, "C4": 1004, "C5": 1005}
     sd = seeds[cfg] if seed is None else seed
     fp = np.zeros(2)
@@ -246,6 +258,9 @@ def make_random(seed: int, b: int, m: int, s: int, tau: int, kind: int = KIND_LA
         A = ((stream(seed, S_A, s * tau) % np.uint64(17)).astype(np.int64) - 8).astype(np.float64).reshape(s, tau)
     else:
         A = (uniform53(seed, S_A, s * tau) * 2.0 - 1.0).reshape(s, tau)
+    if kind == KIND_MC:
+        return Problem(f"rand{seed}", kind, b, m, s, tau, w, None, None, None, None, mapping, A, f,
+                       np.array([0.2, 1.0]), True, seed, mc_seed=seed * 7 + 1)
     if kind == KIND_LATTICE:
         z = draw_z(seed, b, m, w)
         sh = uniform53(seed, S_SHIFT, s) if shifted else None
