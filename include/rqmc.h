@@ -149,6 +149,24 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream);
 
+/* Batched randomisation: R independent randomisations of
+ * the SAME plan (generating vector / matrices, layout, map) and the same A, each giving its own
+ * local f-sum:  d_fsum[r] = sum over this rank's rows of f(x^(r)_k^T A), r = 0..R-1 (device array).
+ * Exactly the input matching the plan's kind is read (host arrays, copied by the call):
+ *   lattice : hshifts  R*s doubles, row r = Delta^(r) in [0,1)^s (plan created with a shift)
+ *   net     : hdshifts R*s words  < 2^53, row r = sigma^(r)        (plan created with a dshift)
+ *   reduced MC: hseeds R seeds (replica r draws with seed hseeds[r]).
+ * Q_N^(r) = (all-reduce of d_fsum[r]) / N; their mean and standard error over r form the RQMC
+ * estimate.  Replica r computes exactly what rqmc_qn computes for a plan holding that shift/seed
+ * (same kernels, same summation order: bit-identical).  Replicas run together (grid dimension) in
+ * chunks of as many as the workspace holds; rqmc_workspace_size_batch(p, R) is the size for all R
+ * at once (>= that of one replica).  Errors: EINVAL (missing input, unshifted plan, workspace below
+ * one replica), ESHIFT (shift outside [0,1) / >= 2^53), ECUDA. */
+rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes);
+rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uint64_t* hdshifts,
+                          const uint64_t* hseeds, const double* dA, int64_t lda, rqmc_f f,
+                          const double* fparam, double* d_fsum, void* dwork, size_t wbytes, void* stream);
+
 /* Debug / parity: the reduced points of level `idx` for local rows [r0, r0+count):
  * d_words[i*s_w+q] = integer word (lattice t = r z'_j mod M; net W or shifted V) and
  * d_vals[i*s_w+q] = the mapped fp64 coordinate.  Either output may be NULL. */

@@ -66,7 +66,7 @@ class Summary(C.Structure):
 EXPORTS = ["rqmc_plan_create", "rqmc_plan_destroy", "rqmc_strerror", "rqmc_plan_last_error",
            "rqmc_plan_summary_get", "rqmc_plan_level", "rqmc_plan_global_row", "rqmc_plan_stats",
            "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_points",
-           "rqmc_profile_enable", "rqmc_profile_read"]
+           "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch"]
 
 _lib = None
 
@@ -97,6 +97,9 @@ def lib():
         L.rqmc_qn_host.argtypes = [vp, dp, i64, C.c_int, dp, dp, vp, C.c_size_t, vp]
         L.rqmc_points.argtypes = [vp, C.c_int, i64, i64, vp, vp, vp]
         L.rqmc_profile_enable.argtypes = [vp, C.c_int]
+        L.rqmc_workspace_size_batch.argtypes = [vp, C.c_int, C.POINTER(C.c_size_t)]
+        L.rqmc_qn_batch.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), vp, i64,
+                                    C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_profile_read.argtypes = [vp, C.POINTER(C.c_int), dp, dp, dp, dp]
         _lib = L
     return _lib
@@ -231,6 +234,51 @@ class Plan:
             import torch.distributed as dist
             dist.all_reduce(part, group=group)
         return float(part.item()) / self.N
+
+    def workspace_size_batch(self, R: int) -> int:
+        n = C.c_size_t()
+        self._check(lib().rqmc_workspace_size_batch(self._h, R, C.byref(n)))
+        return n.value
+
+    def qn_batch(self, A, f: int, fparam=None, shifts=None, dshifts=None, seeds=None, out=None,
+                 max_workspace_bytes: Optional[int] = None, stream=None):
+        """Batched randomisation (rqmc_qn_batch): local f-sums for R shifts (lattice: R x s array),
+        digital shifts (net: R x s words) or seeds (reduced MC: R); returns an R-element device tensor."""
+        import torch
+        self._check_A(A, self.s, self.tau)
+        src = shifts if shifts is not None else (dshifts if dshifts is not None else seeds)
+        if src is None:
+            raise ValueError("qn_batch needs shifts, dshifts or seeds")
+        R = len(src)
+        sh = None if shifts is None else _arr(np.asarray(shifts, dtype=np.float64).reshape(R, self.s), np.float64)
+        ds = None if dshifts is None else _arr(np.asarray(dshifts, dtype=np.uint64).reshape(R, self.s), np.uint64)
+        sd = None if seeds is None else _arr(np.asarray(seeds, dtype=np.uint64).reshape(R), np.uint64)
+        need = self.workspace_size_batch(R)
+        if max_workspace_bytes is not None:
+            need = max(min(need, max_workspace_bytes), self.workspace_size_batch(1))
+        if self._ws is None or self._ws.device != A.device or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=A.device)
+        ws = self._ws
+        out = torch.empty(R, dtype=torch.float64, device=A.device) if out is None else out
+        fp = _arr(fparam if fparam is not None else [0.0, 0.0], np.float64)
+        self._check(lib().rqmc_qn_batch(self._h, R, _p(sh, C.c_double), _p(ds, C.c_uint64), _p(sd, C.c_uint64),
+                                        C.c_void_p(A.data_ptr()), A.stride(0), f, _p(fp, C.c_double),
+                                        C.c_void_p(out.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                        min(ws.numel(), need), _stream_ptr(stream)))
+        return out
+
+    def rqmc_estimate(self, A, f: int, fparam=None, shifts=None, dshifts=None, seeds=None, group=None):
+        """(Q_N mean over the R randomisations, standard error, per-replica Q_N) -- torch.distributed
+        aware like qn(): the per-replica local sums are all-reduced over `group` when initialised."""
+        import torch
+        sums = self.qn_batch(A, f, fparam, shifts=shifts, dshifts=dshifts, seeds=seeds)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(sums, group=group)
+        q = (sums / self.N).cpu().numpy()
+        R = len(q)
+        se = float(np.std(q, ddof=1) / np.sqrt(R)) if R > 1 else float("nan")
+        return float(np.mean(q)), se, q
 
     def qn_host(self, A_host: np.ndarray, f: int, fparam=None, device=None, stream=None) -> float:
         """End-to-end: host A in, host local f-sum out (H2D and D2H inside the C call)."""

@@ -326,6 +326,8 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   c.tg = lane & 3;
   c.t = c.wm * 8 + c.g;
   c.r0 = (int64_t)blockIdx.x * kBundle;
+  const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
+  const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
 
   // X^red of the subtree -> smem [run][q][t] (t stride kPad); global rows r0 + t + j Mroot, read
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     // lane = t (conflict-free smem stores), loop over (run, q) rows, 4 loads in flight per thread
     const int nrow = L.runs * L.K;
     const int t = tid & (kBundle - 1);
-    const double* src = L.X + (c.r0 + t) * L.ldx;
+    const double* src = L.X + rep * a.xrep + (c.r0 + t) * L.ldx;
     for (int r = tid >> 5; r < nrow; r += 4 * (kFineThreads >> 5)) {
       double v[4];
 #pragma unroll
@@ -385,8 +387,8 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     // (tau may be odd: the second element of the last chunk is then masked by a scalar copy)
     for (int e = tid; e < kBundle * (kFineBN / 2); e += kFineThreads) {
       const int t = e / (kFineBN / 2), cc = (e % (kFineBN / 2)) * 2;
-      const bool row_ok = a.root != nullptr && t < c.beff;
-      const double* src = a.root + (c.r0 + t) * a.ldroot + c0 + cc;
+      const bool row_ok = root != nullptr && t < c.beff;
+      const double* src = root + (c.r0 + t) * a.ldroot + c0 + cc;
       if (c0 + cc + 1 < a.tau || !row_ok) {
         cp_async16(rs + t * kPad + cc, row_ok ? src : a.A, row_ok);
       } else {  // last, odd column: copy one element, zero the other
@@ -475,16 +477,16 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < kFineThreads / 32; ++w) t += red[w];
-      a.partial[blockIdx.x] = t;
+      a.partial[rep * a.partrep + blockIdx.x] = t;
     }
   }
 }
 
 template <int NF, class BT>
-static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
+static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   cudaError_t e = set_smem_once(k_fine<NF, BT>, a.smem_bytes);
   if (e != cudaSuccess) return e;
-  k_fine<NF, BT><<<(unsigned)nb, kFineThreads, a.smem_bytes, st>>>(a);
+  k_fine<NF, BT><<<dim3((unsigned)nb, (unsigned)nrep), kFineThreads, a.smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -500,33 +502,33 @@ static bool bottom_matches(const FineArgs& a) {
 }
 
 template <int NF>
-static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, cudaStream_t st) {
+static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   if constexpr (NF >= 3)
-    if (bottom_matches<BotB2>(a)) return launch_fine_t<NF, BotB2>(a, nb, st);
+    if (bottom_matches<BotB2>(a)) return launch_fine_t<NF, BotB2>(a, nb, nrep, st);
   if constexpr (NF >= 2) {
-    if (bottom_matches<BotB2s>(a)) return launch_fine_t<NF, BotB2s>(a, nb, st);
-    if (bottom_matches<BotB3>(a)) return launch_fine_t<NF, BotB3>(a, nb, st);
+    if (bottom_matches<BotB2s>(a)) return launch_fine_t<NF, BotB2s>(a, nb, nrep, st);
+    if (bottom_matches<BotB3>(a)) return launch_fine_t<NF, BotB3>(a, nb, nrep, st);
   }
-  return launch_fine_t<NF, BotNone>(a, nb, st);
+  return launch_fine_t<NF, BotNone>(a, nb, nrep, st);
 }
 
-cudaError_t launch_tree(const FineArgs& a, int64_t nb, cudaStream_t st);
+cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st);
 
-cudaError_t launch_fine(const FineArgs& a, int64_t nb, cudaStream_t st) {
+cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   if (std::getenv("RQMC_NO_TREE") == nullptr) {
-    const cudaError_t e = launch_tree(a, nb, st);
+    const cudaError_t e = launch_tree(a, nb, nrep, st);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (a.NF) {
-    case 0: return launch_fine_t<0, BotNone>(a, nb, st);
-    case 1: return launch_fine_n<1>(a, nb, st);
-    case 2: return launch_fine_n<2>(a, nb, st);
-    case 3: return launch_fine_n<3>(a, nb, st);
-    case 4: return launch_fine_n<4>(a, nb, st);
-    case 5: return launch_fine_n<5>(a, nb, st);
-    case 6: return launch_fine_n<6>(a, nb, st);
-    case 7: return launch_fine_n<7>(a, nb, st);
-    case 8: return launch_fine_n<8>(a, nb, st);
+    case 0: return launch_fine_t<0, BotNone>(a, nb, nrep, st);
+    case 1: return launch_fine_n<1>(a, nb, nrep, st);
+    case 2: return launch_fine_n<2>(a, nb, nrep, st);
+    case 3: return launch_fine_n<3>(a, nb, nrep, st);
+    case 4: return launch_fine_n<4>(a, nb, nrep, st);
+    case 5: return launch_fine_n<5>(a, nb, nrep, st);
+    case 6: return launch_fine_n<6>(a, nb, nrep, st);
+    case 7: return launch_fine_n<7>(a, nb, nrep, st);
+    case 8: return launch_fine_n<8>(a, nb, nrep, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -50,6 +50,10 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
   const int64_t r0 = u * mp_blk + in0;               // first row of the tile
   const int64_t rlim = min(a.M, u * mp_blk + mp_blk);  // rows >= rlim belong to another tile
   const int c0 = blockIdx.x * BN;
+  // replica blockIdx.z (batched randomisation): its own X^red and R buffers, shared A
+  const double* __restrict__ Xg = a.X + (int64_t)blockIdx.z * a.xrep;
+  const double* __restrict__ Rpg = a.Rp ? a.Rp + (int64_t)blockIdx.z * a.rrep : nullptr;
+  double* __restrict__ Rg = a.R + (int64_t)blockIdx.z * a.rrep;
 
   auto load_stage = [&](int buf, int k0) {
     // X tile: BM rows x BK cols (ldx even: 16B chunks stay inside the zero-padded row)
@@ -57,7 +61,7 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
       const int row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
       const int64_t gr = r0 + row;
       const bool ok = gr < rlim && (k0 + kc) < a.ldx;
-      const double* src = ok ? a.X + gr * a.ldx + k0 + kc : a.X;
+      const double* src = ok ? Xg + gr * a.ldx + k0 + kc : Xg;
       cp_async16(&Xs[buf][row][kc], src, ok);
     }
     // A tile: BK rows x BN cols
@@ -86,8 +90,8 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
       acc[i][jn][0] = 0.0;
       acc[i][jn][1] = 0.0;
-      if (a.Rp && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
-        const double* p = a.Rp + (row % a.Mp) * a.ldp + col;
+      if (Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
+        const double* p = Rpg + (row % a.Mp) * a.ldp + col;
         if (CH == 2 && col + 1 < a.tau) {
           const double2 v = *reinterpret_cast<const double2*>(p);
           acc[i][jn][0] = v.x;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
-      double* p = a.R + row * a.ldr + col;
+      double* p = Rg + row * a.ldr + col;
       if (col + 1 < a.tau) {
         *reinterpret_cast<double2*>(p) = make_double2(acc[i][jn][0], acc[i][jn][1]);
       } else if (col < a.tau) {
@@ -138,8 +142,8 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
   }
 }
 
-cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
-  if (a.M == 0) return cudaSuccess;
+cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
+  if (a.M == 0 || nrep == 0) return cudaSuccess;
   const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
                    (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
   const int BM = a.M >= 64 * 148 ? 128 : 64;
@@ -156,7 +160,8 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     // grid.x = column blocks (fastest: the 32 CTAs of one row block share its X^red rows in L2)
     for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
-      dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0));
+      dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0),
+                (unsigned)nrep);
       kern<<<grid, nt, sm, st>>>(a, mp_blk, nu, y0);
     }
     return cudaGetLastError();

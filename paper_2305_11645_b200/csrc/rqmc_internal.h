@@ -21,6 +21,7 @@ struct GenLevel {
   int64_t Ml;     // local rows
   int64_t xoff;   // offset (doubles) of X^red in the workspace
   int j_lo, s_w, ldx, pad;
+  double inv_M;   // 2^-(m-w) for b = 2 (exact scaling of t / M)
 };
 
 struct GenArgs {
@@ -31,6 +32,11 @@ struct GenArgs {
   const uint64_t* C;             // net column words (row-zeroed)
   const uint64_t* dshift;        // net sigma_j
   uint64_t seed;                 // reduced MC generator seed
+  // replicas (batched randomisation, NEXT-2): replica r = blockIdx.z uses shift[r*srep + j] /
+  // dshift[r*srep + j] / seeds[r] (seeds NULL: seed) and writes X + r*xrep
+  int srep;
+  int64_t xrep;
+  const uint64_t* seeds;
   double* X;                     // workspace base
   GenLevel lv[kMaxLevels];
 };
@@ -43,6 +49,7 @@ struct GemmArgs {                // one coarse level: R = tile(Rp) + X A_w
   int tau;
   const double* Rp; int64_t ldp; int64_t Mp;   // parent R (nullptr: zero)
   double* R; int64_t ldr;
+  int64_t xrep, rrep;            // replica strides (doubles) of X and of the R buffers (grid.z = replica)
 };
 
 struct FineLevel {
@@ -62,13 +69,14 @@ struct FineArgs {
   int root_off;       // root tile buffers offset (doubles), 2 x kBundle x kFinePad
   int acc_off;        // rowacc offset (doubles)
   int smem_bytes;
+  int64_t xrep, rootrep, partrep;  // replica strides (doubles): X^red, root R, partials (grid.y = replica)
 };
 
-cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, cudaStream_t st);
+cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, int nrep, cudaStream_t st);
 cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, uint64_t* words,
                           double* vals, cudaStream_t st);
-cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
-cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, cudaStream_t st);
-cudaError_t launch_reduce(const double* partial, int64_t n, double* out, cudaStream_t st);
+cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st);
+cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, int nrep, cudaStream_t st);
+cudaError_t launch_reduce(const double* partial, int64_t n, int64_t stride, int nrep, double* out, cudaStream_t st);
 
 }  // namespace rqmc

@@ -402,7 +402,7 @@ GenArgs gen_args(const rqmc_plan_s* p, void* work) {
   g.X = reinterpret_cast<double*>(static_cast<char*>(work) + p->off_x);
   for (size_t i = 0; i < p->lv.size(); ++i) {
     const Level& L = p->lv[i];
-    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, 0};
+    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, 0, std::ldexp(1.0, -(p->m - L.w))};
   }
   return g;
 }
@@ -412,25 +412,30 @@ rqmc_status check_cuda(rqmc_plan_s* p, cudaError_t e, const char* what) {
   return fail(p, RQMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
-                const double* fparam, double* d_fsum, void* dwork, size_t wbytes, cudaStream_t st) {
-  if (!p || !dA || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
-  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->total));
-  if (lda < p->tau || (dY && ldy < p->tau)) return fail(p, RQMC_EDIM, "lda/ldy < tau");
-  if (f < RQMC_F_NONE || f > RQMC_F_MEAN) return fail(p, RQMC_EINVAL, "bad f");
-  if (f == RQMC_F_CALL_MEAN_EXP && !fparam) return fail(p, RQMC_EINVAL, "f needs fparam");
+// One pass of the hot path for nrep replicas (batched randomisation) whose workspace slices of
+// rep_bytes each start at `base`: replica r uses shift[r*srep + j] / dshift[...] / seeds[r].
+// nrep = 1 with the plan's own tables is the plain run.
+struct RunRand {
+  const double* shift;
+  const uint64_t* dshift;
+  const uint64_t* seeds;
+  int srep;
+};
+
+rqmc_status run_core(rqmc_plan_s* p, int nrep, char* w, size_t rep_bytes, const RunRand& rr, const double* dA,
+                     int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
+                     cudaStream_t st) {
   const bool want_f = f != RQMC_F_NONE && d_fsum;
-  if (!want_f && !dY) return RQMC_OK;
-  if (rqmc_status s = upload(p)) return s;
-  char* w = static_cast<char*>(dwork);
   cudaEvent_t* ev = nullptr;
   if (p->prof_runs < p->prof_max) ev = &p->prof_ev[5 * p->prof_runs++];
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
+  const int64_t rep_d = (int64_t)(rep_bytes / sizeof(double));
   mark(0);
 
-  // a2: reduced points of every level
-  GenArgs g = gen_args(p, dwork);
-  if (rqmc_status s = check_cuda(p, launch_gen(g, p->max_gen_entries, st), "k_gen")) return s;
+  // a2: reduced points of every level (all replicas: grid.z)
+  GenArgs g = gen_args(p, w);
+  g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
+  if (rqmc_status s = check_cuda(p, launch_gen(g, p->max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
 
   // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine
@@ -444,7 +449,8 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
       a.Rp = reinterpret_cast<const double*>(w + p->off_r[P.rbuf]); a.ldp = p->ldr; a.Mp = P.Ml;
     }
     a.R = reinterpret_cast<double*>(w + p->off_r[L.rbuf]); a.ldr = p->ldr;
-    if (rqmc_status s = check_cuda(p, launch_gemm(a, st), "k_level_gemm")) return s;
+    a.xrep = rep_d; a.rrep = rep_d;
+    if (rqmc_status s = check_cuda(p, launch_gemm(a, nrep, st), "k_level_gemm")) return s;
   }
 
   mark(2);
@@ -475,12 +481,40 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   fa.root_off = 2 * p->fine_as_stride;
   fa.acc_off = p->fine_acc_off;
   fa.smem_bytes = p->fine_smem;
-  if (rqmc_status s = check_cuda(p, launch_fine(fa, p->nbundles, st), "k_fine")) return s;
+  fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
+  if (rqmc_status s = check_cuda(p, launch_fine(fa, p->nbundles, nrep, st), "k_fine")) return s;
   mark(3);
   if (want_f)
-    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, p->nbundles, d_fsum, st), "k_reduce")) return s;
+    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, p->nbundles, rep_d, nrep, d_fsum, st), "k_reduce"))
+      return s;
   mark(4);
   return RQMC_OK;
+}
+
+rqmc_status check_f(rqmc_plan_s* p, rqmc_f f, const double* fparam) {
+  if (f < RQMC_F_NONE || f > RQMC_F_MEAN) return fail(p, RQMC_EINVAL, "bad f");
+  if (f == RQMC_F_CALL_MEAN_EXP && !fparam) return fail(p, RQMC_EINVAL, "f needs fparam");
+  return RQMC_OK;
+}
+
+rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                const double* fparam, double* d_fsum, void* dwork, size_t wbytes, cudaStream_t st) {
+  if (!p || !dA || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->total));
+  if (lda < p->tau || (dY && ldy < p->tau)) return fail(p, RQMC_EDIM, "lda/ldy < tau");
+  if (rqmc_status s = check_f(p, f, fparam)) return s;
+  const bool want_f = f != RQMC_F_NONE && d_fsum;
+  if (!want_f && !dY) return RQMC_OK;
+  if (rqmc_status s = upload(p)) return s;
+  const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
+  return run_core(p, 1, static_cast<char*>(dwork), p->off_fsum, rr, dA, lda, dY, ldy, f, fparam, d_fsum, st);
+}
+
+// bytes of one replica's workspace slice [X^red][R0][R1][partials] and of a chunk of n replicas
+size_t rep_slice_bytes(const rqmc_plan_s* p) { return p->off_fsum; }
+size_t batch_bytes(const rqmc_plan_s* p, int64_t n) {
+  const size_t tab = (p->kind == RQMC_REDUCED_MC ? 1 : (size_t)p->s) * sizeof(double);
+  return (size_t)n * rep_slice_bytes(p) + align_up((size_t)n * tab, 256);
 }
 
 }  // namespace
@@ -514,6 +548,61 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
   e = cudaMemcpyAsync(h_fsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   return check_cuda(p, e, "D2H fsum");
+}
+
+rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes) {
+  if (!p || !bytes || R < 1) return RQMC_EINVAL;
+  *bytes = batch_bytes(p, R);
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uint64_t* hdshifts,
+                          const uint64_t* hseeds, const double* dA, int64_t lda, rqmc_f f, const double* fparam,
+                          double* d_fsum, void* dwork, size_t wbytes, void* stream) {
+  if (!p || !dA || !dwork || !d_fsum || R < 1) return fail(p, RQMC_EINVAL, "null pointer or R < 1");
+  if (f == RQMC_F_NONE) return fail(p, RQMC_EINVAL, "rqmc_qn_batch needs f");
+  if (lda < p->tau) return fail(p, RQMC_EDIM, "lda < tau");
+  if (rqmc_status s = check_f(p, f, fparam)) return s;
+  const void* tab = nullptr;
+  size_t per = (size_t)p->s * sizeof(double);
+  if (p->kind == RQMC_LATTICE) {
+    if (!hshifts || !p->shifted) return fail(p, RQMC_EINVAL, "lattice batch needs hshifts and a shifted plan");
+    for (int64_t i = 0; i < (int64_t)R * p->s; ++i)
+      if (!(hshifts[i] >= 0.0 && hshifts[i] < 1.0))
+        return fail(p, RQMC_ESHIFT, "batch shift " + std::to_string(i / p->s) + "," + std::to_string(i % p->s) +
+                                        " outside [0,1)");
+    tab = hshifts;
+  } else if (p->kind == RQMC_DIGITAL_NET) {
+    if (!hdshifts || !p->shifted) return fail(p, RQMC_EINVAL, "net batch needs hdshifts and a shifted plan");
+    for (int64_t i = 0; i < (int64_t)R * p->s; ++i)
+      if (hdshifts[i] >> 53) return fail(p, RQMC_ESHIFT, "batch digital shift >= 2^53");
+    tab = hdshifts;
+  } else {
+    if (!hseeds) return fail(p, RQMC_EINVAL, "reduced-MC batch needs hseeds");
+    tab = hseeds;
+    per = sizeof(uint64_t);
+  }
+  int64_t chunk = R;
+  while (chunk > 0 && batch_bytes(p, chunk) > wbytes) --chunk;
+  if (chunk == 0) return fail(p, RQMC_EINVAL, "workspace too small for one replica: need " +
+                                                  std::to_string(batch_bytes(p, 1)));
+  if (rqmc_status s = upload(p)) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(dwork);
+  for (int64_t r0 = 0; r0 < R; r0 += chunk) {
+    const int n = (int)std::min<int64_t>(chunk, R - r0);
+    char* dtab = w + (size_t)chunk * rep_slice_bytes(p);
+    cudaError_t e = cudaMemcpyAsync(dtab, static_cast<const char*>(tab) + (size_t)r0 * per, (size_t)n * per,
+                                    cudaMemcpyHostToDevice, st);
+    if (rqmc_status s = check_cuda(p, e, "H2D batch shifts")) return s;
+    RunRand rr{nullptr, nullptr, nullptr, p->s};
+    if (p->kind == RQMC_LATTICE) rr.shift = reinterpret_cast<const double*>(dtab);
+    else if (p->kind == RQMC_DIGITAL_NET) rr.dshift = reinterpret_cast<const uint64_t*>(dtab);
+    else rr.seeds = reinterpret_cast<const uint64_t*>(dtab);
+    if (rqmc_status s = run_core(p, n, w, rep_slice_bytes(p), rr, dA, lda, nullptr, 0, f, fparam, d_fsum + r0, st))
+      return s;
+  }
+  return RQMC_OK;
 }
 
 rqmc_status rqmc_points(rqmc_plan_t p, int idx, int64_t r0, int64_t count, uint64_t* d_words, double* d_vals,

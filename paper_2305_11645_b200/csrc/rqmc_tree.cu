@@ -363,13 +363,15 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
   c.cw = c.ch * 8 * NFR;
   c.r0 = (int64_t)blockIdx.x * kBundle;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
+  const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
+  const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
 
   // X^red of the subtree -> smem [level][run][q][t]: the bundle's rows of one run are 32 K contiguous
   // doubles in HBM, read coalesced by 8-byte cp.async and transposed on the way into smem
 #pragma unroll
   for (int i = 0; i < NF; ++i) {
     const int K = T::K(i), n = T::runs(i) * kBundle * K;
-    const double* src = a.lv[i].X + c.r0 * (int64_t)K;
+    const double* src = a.lv[i].X + rep * a.xrep + c.r0 * (int64_t)K;
     double* dst = fsm + T::XS + i * T::XL;
     for (int e = tid; e < n; e += NT) {
       const int j = e / (kBundle * K), r = e - j * (kBundle * K), t = r / K, q = r - t * K;
@@ -403,8 +405,8 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
     }
     for (int e = tid; e < kBundle * (kFineBN / 2); e += NT) {
       const int t = e >> 4, cc = (e & 15) * 2;
-      const bool row_ok = a.root != nullptr && t < c.beff;
-      const double* src = a.root + (c.r0 + t) * a.ldroot + c0 + cc;
+      const bool row_ok = root != nullptr && t < c.beff;
+      const double* src = root + (c.r0 + t) * a.ldroot + c0 + cc;
       if (c0 + cc + 1 < a.tau || !row_ok) {
         cp_async16(rs + t * kPad + cc, row_ok ? src : a.A, row_ok);
       } else {
@@ -471,13 +473,13 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t += red[w];
-      a.partial[blockIdx.x] = t;
+      a.partial[rep * a.partrep + blockIdx.x] = t;
     }
   }
 }
 
 template <int NF, int B, int G, bool STY>
-static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, cudaStream_t st) {
+static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   constexpr int NFR = RQMC_TREE_NFR;
   using T = Tree<NF, B, NFR>;
   if constexpr (T::SMEM > 227 * 1024) {
@@ -485,7 +487,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, cudaStream_t st)
   }
   cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR>, T::SMEM);
   if (e != cudaSuccess) return e;
-  k_fine_tree<NF, B, G, STY, NFR><<<(unsigned)nb, T::THREADS, T::SMEM, st>>>(a);
+  k_fine_tree<NF, B, G, STY, NFR><<<dim3((unsigned)nb, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -502,27 +504,27 @@ static bool tree_matches(const FineArgs& a) {
 }
 
 template <int NF, int B>
-static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, cudaStream_t st) {
+static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   const bool sty = a.Y != nullptr;
   switch (a.fk) {
-    case -1: return launch_tree_t<NF, B, 0, true>(a, nb, st);
-    case 1: return sty ? launch_tree_t<NF, B, 2, true>(a, nb, st) : launch_tree_t<NF, B, 2, false>(a, nb, st);
-    case 2: return sty ? launch_tree_t<NF, B, 3, true>(a, nb, st) : launch_tree_t<NF, B, 3, false>(a, nb, st);
-    default: return sty ? launch_tree_t<NF, B, 1, true>(a, nb, st) : launch_tree_t<NF, B, 1, false>(a, nb, st);
+    case -1: return launch_tree_t<NF, B, 0, true>(a, nb, nrep, st);
+    case 1: return sty ? launch_tree_t<NF, B, 2, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 2, false>(a, nb, nrep, st);
+    case 2: return sty ? launch_tree_t<NF, B, 3, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 3, false>(a, nb, nrep, st);
+    default: return sty ? launch_tree_t<NF, B, 1, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 1, false>(a, nb, nrep, st);
   }
 }
 
 // returns cudaErrorNotSupported when no compile-time tree matches
-cudaError_t launch_tree(const FineArgs& a, int64_t nb, cudaStream_t st) {
+cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   if (a.Y == nullptr && a.fk < 0) return cudaErrorNotSupported;
-  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, st);
-  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, st);
-  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, st);
-  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, st);
-  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, st);
-  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, st);
-  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, st);
-  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, st);
+  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, nrep, st);
+  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, nrep, st);
+  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, nrep, st);
+  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, nrep, st);
+  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, nrep, st);
+  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, nrep, st);
+  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, nrep, st);
+  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, nrep, st);
   return cudaErrorNotSupported;
 }
 

@@ -1,0 +1,94 @@
+"""Batched randomisation: R independent shifts
+(lattice), digital shifts (net) or seeds (reduced MC) of one plan and one A, run together.
+
+Bars: replica r is BIT-IDENTICAL to a plain rqmc_qn run of a plan holding that randomisation (same
+kernels, same summation order), and within relative 1e-12 of the oracle's Q_N sum.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from test_gpu_parity import dev, rq  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _replicas(prob, R, seed):
+    rng = np.random.default_rng(seed)
+    if prob.kind == W.KIND_LATTICE:
+        return {"shifts": rng.random((R, prob.s))}
+    if prob.kind == W.KIND_NET:
+        return {"dshifts": rng.integers(0, 1 << 53, size=(R, prob.s), dtype=np.uint64)}
+    return {"seeds": rng.integers(0, 1 << 63, size=R, dtype=np.uint64)}
+
+
+def _with(prob, kw, r):
+    import dataclasses
+    if "shifts" in kw:
+        return dataclasses.replace(prob, shift=kw["shifts"][r])
+    if "dshifts" in kw:
+        return dataclasses.replace(prob, dshift=kw["dshifts"][r])
+    return dataclasses.replace(prob, mc_seed=int(kw["seeds"][r]))
+
+
+@pytest.mark.parametrize("seed,b,m,s,tau,kind,mapping,f,R", [
+    (1, 2, 11, 64, 70, W.KIND_LATTICE, W.MAP_INVNORM, W.F_EXP_MEAN, 5),
+    (2, 3, 7, 90, 33, W.KIND_LATTICE, W.MAP_INVNORM, W.F_CALL_MEAN_EXP, 4),
+    (3, 2, 10, 100, 40, W.KIND_NET, W.MAP_UNIT, W.F_MEAN_SQ, 3),
+    (4, 2, 12, 130, 64, W.KIND_MC, W.MAP_INVNORM, W.F_EXP_MEAN, 6),
+])
+def test_batch_equals_single_runs_and_oracle(rq, seed, b, m, s, tau, kind, mapping, f, R):
+    prob = W.make_random(seed, b, m, s, tau, kind=kind, shifted=kind != W.KIND_MC, mapping=mapping, f=f)
+    kw = _replicas(prob, R, seed)
+    A = dev(prob.A)
+    pl = rq.Plan.from_problem(prob)
+    sums = pl.qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
+    for r in range(R):
+        pr = _with(prob, kw, r)
+        single = float(rq.Plan.from_problem(pr).qn_sum(A, prob.f, prob.fparam).item())
+        assert sums[r] == single, (r, sums[r], single)
+        fo = oracle.f_rows(pr, np.arange(pr.N))
+        assert abs(sums[r] - oracle.neumaier(fo)) <= 1e-12 * np.abs(fo).sum()
+
+
+def test_batch_chunking_identical(rq):
+    """A workspace for 2 replicas processes R = 7 in chunks; results identical to one launch of 7."""
+    prob = W.make_random(9, 2, 12, 80, 50, shifted=True, mapping=W.MAP_INVNORM)
+    kw = _replicas(prob, 7, 9)
+    A = dev(prob.A)
+    full = rq.Plan.from_problem(prob).qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
+    pl = rq.Plan.from_problem(prob)
+    small = pl.qn_batch(A, prob.f, prob.fparam, max_workspace_bytes=pl.workspace_size_batch(2), **kw).cpu().numpy()
+    assert np.array_equal(full, small)
+
+
+def test_batch_c2_rqmc_estimate(rq):
+    """C2 (the paper's Asian-option shape) with R = 16 random shifts: every replica equals its plain
+    run bit for bit; the RQMC mean/stderr are consistent with the replicas."""
+    prob = W.make_config("C2")
+    kw = _replicas(prob, 16, 2)
+    A = dev(prob.A)
+    pl = rq.Plan.from_problem(prob)
+    mean, se, q = pl.rqmc_estimate(A, prob.f, prob.fparam, **kw)
+    for r in (0, 7, 15):
+        single = float(rq.Plan.from_problem(_with(prob, kw, r)).qn_sum(A, prob.f, prob.fparam).item())
+        assert q[r] == single / prob.N
+    assert mean == pytest.approx(np.mean(q), rel=1e-15) and se > 0 and se < 0.1 * abs(mean)
+
+
+def test_batch_errors(rq):
+    prob = W.make_random(5, 2, 8, 20, 8)                  # unshifted lattice plan
+    A = dev(prob.A)
+    pl = rq.Plan.from_problem(prob)
+    with pytest.raises(rq.RqmcError) as e:
+        pl.qn_batch(A, prob.f, prob.fparam, shifts=np.zeros((2, 20)))
+    assert e.value.code == 1
+    prob = W.make_random(5, 2, 8, 20, 8, shifted=True)
+    pl = rq.Plan.from_problem(prob)
+    bad = np.zeros((2, 20))
+    bad[1, 3] = 1.0
+    with pytest.raises(rq.RqmcError) as e:
+        pl.qn_batch(A, prob.f, prob.fparam, shifts=bad)
+    assert e.value.code == 5
