@@ -163,6 +163,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="R > 1: batched randomisation (rqmc_qn_batch) of R shifts / seeds per step")
     args = ap.parse_args()
     prob = W.make_config(args.config)
     if args.impl == "reference":
@@ -189,11 +191,23 @@ def main():
     stream = torch.cuda.current_stream()
 
     Y = None
-    if prob.store_y:   # configs whose output is the full XA (C1, C4): Y written to HBM every step
+    if prob.store_y and args.replicas == 1:   # configs whose output is the full XA (C1, C4): Y written every step
         Y = torch.empty((prob.N // world, prob.tau), dtype=torch.float64, device="cuda")
+    R = args.replicas
+    rkw = {}
+    if R > 1:   # R independent randomisations of the same plan
+        if prob.kind == W.KIND_LATTICE:
+            rkw = {"shifts": W.uniform53(prob.seed, 77, R * prob.s).reshape(R, prob.s)}
+        elif prob.kind == W.KIND_NET:
+            rkw = {"dshifts": (W.stream(prob.seed, 77, R * prob.s) >> np.uint64(11)).reshape(R, prob.s)}
+        else:
+            rkw = {"seeds": W.stream(prob.seed, 77, R)}
+        fsum = torch.zeros(R, dtype=torch.float64, device="cuda")
 
     def step():
-        if Y is not None:
+        if R > 1:
+            plan.qn_batch(A, prob.f, prob.fparam, out=fsum, **rkw)
+        elif Y is not None:
             plan.xa(A, prob.f, prob.fparam, Y=Y, fsum=fsum)
         else:
             plan.qn_sum(A, prob.f, prob.fparam, out=fsum)
@@ -231,7 +245,7 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    qn_val = float(fsum.item()) / prob.N
+    qn_val = float(fsum.mean().item()) / prob.N
 
     # ---- end-to-end through the public API with host buffers (pinned A in, f-sum out)
     A_pin = torch.from_numpy(prob.A.copy()).pin_memory()
@@ -239,6 +253,10 @@ def main():
     A_e2e = torch.empty_like(A)
 
     def e2e_call():
+        if R > 1:       # batched: H2D of A, R f-sums back
+            A_e2e.copy_(A_pin, non_blocking=True)
+            plan.qn_batch(A_e2e, prob.f, prob.fparam, out=fsum, **rkw)
+            return fsum.cpu().numpy()
         if Y is None:   # C ABI rqmc_qn_host: H2D of A and D2H of the f-sum inside the call
             return plan.qn_host(A_host, prob.f, prob.fparam)
         A_e2e.copy_(A_pin, non_blocking=True)   # XA configs: Y stays a device-resident output
@@ -255,9 +273,9 @@ def main():
         t0 = time.perf_counter()
         part = e2e_call()
         if world > 1:
-            pt = torch.tensor([part], dtype=torch.float64, device="cuda")
+            pt = torch.tensor(np.atleast_1d(part), dtype=torch.float64, device="cuda")
             dist.all_reduce(pt)
-            part = float(pt.item())
+            part = pt.cpu().numpy()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -266,9 +284,11 @@ def main():
 
     # ---- roofline of the dominant kernel (k_fine: fused fine levels on the fp64 DFMA pipe)
     levels = plan.levels()
+    if R > 1:
+        summ = plan.summary_batch(R)
     ck = summ["checkpoint"]
-    fine_flops = 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[ck + 1:])
-    coarse_flops = 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[:ck + 1])
+    fine_flops = R * 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[ck + 1:])
+    coarse_flops = R * 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[:ck + 1])
     runs = max(1, prof["runs"])
     fine_ms = prof["fine_ms"] / runs
     coarse_ms = prof["coarse_ms"] / runs
@@ -297,7 +317,7 @@ def main():
     else:
         ach = coarse_flops / (coarse_ms * 1e-3) / 1e12
         bound = "tensor"
-    total_flops = 2.0 * plan.stats()["macs"]
+    total_flops = R * 2.0 * plan.stats()["macs"]
 
     # whole-step roofline: t_roof = max(F / P64, B / BW), F = 2 tau sum_w M_w s_w,
     # B = 8 s tau (A read once) + 8 N tau when Y is stored
@@ -317,7 +337,7 @@ def main():
     launches_per_step = 1 + n_coarse + 1 + 1   # k_gen + coarse GEMMs + k_fine + k_reduce
     line = {
         "metric": METRIC,
-        "value": prob.N * prob.tau / (ms_max / args.steps * 1e-3),
+        "value": R * prob.N * prob.tau / (ms_max / args.steps * 1e-3),
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
@@ -331,14 +351,15 @@ def main():
         "config": {"workload": describe(prob), "N": prob.N, "s": prob.s, "tau": prob.tau,
                    "parallelism": f"residue classes k mod {world}" if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write, outside the step events)",
-                   "checkpoint_w": levels[ck]["w"], "fused_fine_levels": summ["n_fine"]},
+                   "checkpoint_w": levels[ck]["w"], "fused_fine_levels": summ["n_fine"],
+                   "replicas": R},
         "roofline": {"kernel": dominant, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                      "frac": ach / peak, "traffic": traffic, "peak_note": peak_note,
                      ("algorithmic_bytes_per_launch" if unit == "GB/s" else "algorithmic_flops_per_launch"): algo},
         "step_roofline": step_roof,
         "phases_ms_per_step": {k: v / runs for k, v in prof.items() if k.endswith("_ms")},
-        "e2e": {"value": prob.N * prob.tau / (e2e_tot / args.steps * 1e-3), "unit": UNIT,
-                "h2d_bytes_per_step": int(prob.s * prob.tau * 8), "d2h_bytes_per_step": 8,
+        "e2e": {"value": R * prob.N * prob.tau / (e2e_tot / args.steps * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(prob.s * prob.tau * 8), "d2h_bytes_per_step": 8 * R,
                 "api": "rqmc_qn_host (pinned host A -> device, local f-sum -> host)" if Y is None else
                        "Plan.xa (pinned host A -> device copy, Y device-resident output, f-sum -> host)"},
         "gpu_launches": launches_per_step * args.steps,

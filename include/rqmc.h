@@ -157,12 +157,17 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
  *   net     : hdshifts R*s words  < 2^53, row r = sigma^(r)        (plan created with a dshift)
  *   reduced MC: hseeds R seeds (replica r draws with seed hseeds[r]).
  * Q_N^(r) = (all-reduce of d_fsum[r]) / N; their mean and standard error over r form the RQMC
- * estimate.  Replica r computes exactly what rqmc_qn computes for a plan holding that shift/seed
- * (same kernels, same summation order: bit-identical).  Replicas run together (grid dimension) in
+ * estimate.  Replica r computes what rqmc_qn computes for a plan holding that shift/seed -- bit for
+ * bit when the batch runs with the single-run layout (same checkpoint, rqmc_plan_summary_batch),
+ * else up to summation order.  Replicas run together (grid dimension) in
  * chunks of as many as the workspace holds; rqmc_workspace_size_batch(p, R) is the size for all R
  * at once (>= that of one replica).  Errors: EINVAL (missing input, unshifted plan, workspace below
  * one replica), ESHIFT (shift outside [0,1) / >= 2^53), ECUDA. */
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes);
+/* The layout a batch of R concurrent replicas uses: replicas add parallelism, so the checkpoint may
+ * sit coarser (more fused fine levels) than for a single run (summary fields checkpoint, n_fine,
+ * n_bundles; the rest as rqmc_plan_summary_get). */
+rqmc_status rqmc_plan_summary_batch(rqmc_plan_t p, int R, rqmc_plan_summary* out);
 rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uint64_t* hdshifts,
                           const uint64_t* hseeds, const double* dA, int64_t lda, rqmc_f f,
                           const double* fparam, double* d_fsum, void* dwork, size_t wbytes, void* stream);

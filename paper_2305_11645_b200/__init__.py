@@ -66,7 +66,8 @@ class Summary(C.Structure):
 EXPORTS = ["rqmc_plan_create", "rqmc_plan_destroy", "rqmc_strerror", "rqmc_plan_last_error",
            "rqmc_plan_summary_get", "rqmc_plan_level", "rqmc_plan_global_row", "rqmc_plan_stats",
            "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_points",
-           "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch"]
+           "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch",
+           "rqmc_plan_summary_batch"]
 
 _lib = None
 
@@ -98,6 +99,7 @@ def lib():
         L.rqmc_points.argtypes = [vp, C.c_int, i64, i64, vp, vp, vp]
         L.rqmc_profile_enable.argtypes = [vp, C.c_int]
         L.rqmc_workspace_size_batch.argtypes = [vp, C.c_int, C.POINTER(C.c_size_t)]
+        L.rqmc_plan_summary_batch.argtypes = [vp, C.c_int, C.POINTER(Summary)]
         L.rqmc_qn_batch.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), vp, i64,
                                     C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_profile_read.argtypes = [vp, C.POINTER(C.c_int), dp, dp, dp, dp]
@@ -234,6 +236,12 @@ class Plan:
             import torch.distributed as dist
             dist.all_reduce(part, group=group)
         return float(part.item()) / self.N
+
+    def summary_batch(self, R: int) -> dict:
+        """Summary of the layout a batch of R replicas runs with (checkpoint may differ from summary())."""
+        o = Summary()
+        self._check(lib().rqmc_plan_summary_batch(self._h, R, C.byref(o)))
+        return o.as_dict()
 
     def workspace_size_batch(self, R: int) -> int:
         n = C.c_size_t()

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -29,6 +30,19 @@ struct Level {
   int ldx;
   int64_t xoff;   // doubles
   int rbuf;       // coarse: which R buffer
+};
+
+// Everything that depends on the checkpoint level: which levels are coarse, X^red strides and
+// offsets, R buffers, fine-kernel shared-memory layout, workspace offsets.
+struct Layout {
+  int ckpt = -1, nfine = 0;
+  int64_t nbundles = 0;
+  std::vector<Level> lv;     // copy of the plan's levels with coarse / ldx / xoff / rbuf filled
+  int ldr = 0;               // row stride of R buffers
+  size_t off_x = 0, off_r[2] = {0, 0}, off_part = 0, off_a = 0, off_fsum = 0, total = 0;
+  int64_t max_gen_entries = 0;
+  int fine_smem = 0, fine_as_stride = 0, fine_acc_off = 0, leafruns = 1;
+  std::vector<int> fine_xs_off, fine_as_off;
 };
 
 int64_t ipow(int64_t b, int e) {
@@ -59,15 +73,10 @@ struct rqmc_plan_s {
   std::vector<int32_t> w;
   std::vector<uint64_t> z, C, dshift;
   std::vector<double> shift;
-  std::vector<Level> lv;     // coarse -> fine
-  int ckpt = 0, nfine = 0;
-  int64_t nbundles = 0;
-  int ldr = 0;               // row stride of R buffers
-  size_t off_x = 0, off_r[2] = {0, 0}, off_part = 0, off_a = 0, off_fsum = 0, total = 0;
-  int64_t max_gen_entries = 0;
-  // fine-kernel shared-memory layout
-  int fine_smem = 0, fine_as_stride = 0, fine_acc_off = 0, leafruns = 1;
-  std::vector<int> fine_xs_off, fine_as_off;
+  std::vector<Level> lv;     // coarse -> fine (checkpoint-independent fields)
+  Layout L1;                 // layout of single runs (and the default workspace)
+  std::mutex lay_mu;         // batch layouts (deeper checkpoints when replicas add parallelism)
+  std::vector<std::unique_ptr<Layout>> lay_cache;
   // device tables (uploaded once, lazily)
   std::once_flag up_once;
   cudaError_t up_err = cudaSuccess;
@@ -121,6 +130,77 @@ int fine_smem_bytes(const rqmc_plan_s& p, int c, std::vector<int>* xs_off, std::
 }
 
 constexpr int kFineSmemLimit = 200 * 1024;
+
+// Checkpoint choice: the most fused fine levels subject to depth <= kMaxFine, shared memory, and at
+// least 2 waves of fine CTAs (bundles x replicas >= 2 x 148 SMs) -- replicas of a batched run add
+// parallelism, so a batch may fuse more levels than a single run of the same plan.
+int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
+  const int nl = (int)p.lv.size();
+  int best = -1;
+  for (int c = 0; c < nl; ++c) {
+    const int nf = nl - 1 - c;
+    if (nf > kMaxFine) continue;
+    if (fine_smem_bytes(p, c, nullptr, nullptr, nullptr, nullptr, nullptr) > kFineSmemLimit) continue;
+    const int64_t nb = (p.lv[c].Ml + kBundle - 1) / kBundle;
+    if (best < 0) best = c;
+    if (nb * reps >= 2 * 148) { best = c; break; }
+    best = c;  // keep moving finer while parallelism is insufficient
+  }
+  if (const char* env = std::getenv("RQMC_CKPT_W")) {  // tuning override: checkpoint at level w
+    const int wv = std::atoi(env);
+    for (int c = 0; c < nl; ++c)
+      if (p.lv[c].w == wv && nl - 1 - c <= kMaxFine &&
+          fine_smem_bytes(p, c, nullptr, nullptr, nullptr, nullptr, nullptr) <= kFineSmemLimit)
+        best = c;
+  }
+  return best;
+}
+
+// Workspace layout for checkpoint c: [X^red of every level][R buf 0][R buf 1][partials] (one
+// replica's slice, off_fsum bytes) then [f-sum][A staging] for the host entry point.
+void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
+  const int nl = (int)p.lv.size();
+  L.ckpt = c;
+  L.nfine = nl - 1 - c;
+  L.lv = p.lv;
+  for (int i = 0; i < nl; ++i) L.lv[i].coarse = i <= c;
+  L.nbundles = (L.lv[c].Ml + kBundle - 1) / kBundle;
+  L.fine_smem = fine_smem_bytes(p, c, &L.fine_xs_off, &L.fine_as_off, &L.fine_as_stride, &L.fine_acc_off,
+                                &L.leafruns);
+  size_t off = 0;
+  L.off_x = 0;
+  L.max_gen_entries = 0;
+  for (auto& V : L.lv) {
+    V.ldx = V.coarse ? (V.s_w + 1) / 2 * 2 : V.s_w;
+    V.xoff = (int64_t)(off / sizeof(double));
+    off = align_up(off + (size_t)V.Ml * V.ldx * sizeof(double), 256);
+    L.max_gen_entries = std::max<int64_t>(L.max_gen_entries, V.Ml * V.ldx);
+  }
+  L.ldr = (p.tau + 1) / 2 * 2;
+  size_t rsz[2] = {0, 0};
+  for (int i = 0; i <= c; ++i) {
+    L.lv[i].rbuf = i & 1;
+    rsz[i & 1] = std::max(rsz[i & 1], (size_t)L.lv[i].Ml * L.ldr * sizeof(double));
+  }
+  L.off_r[0] = off; off = align_up(off + rsz[0], 256);
+  L.off_r[1] = off; off = align_up(off + rsz[1], 256);
+  L.off_part = off; off = align_up(off + (size_t)L.nbundles * sizeof(double), 256);
+  L.off_fsum = off; off = align_up(off + sizeof(double), 256);
+  L.off_a = off; off = align_up(off + (size_t)p.s * L.ldr * sizeof(double), 256);
+  L.total = off;
+}
+
+// Layout for a batch of `reps` concurrent replicas (cached; the single-run layout when equal).
+const Layout& layout_for(rqmc_plan_s* p, int64_t reps) {
+  const int c = choose_ckpt(*p, reps);
+  if (c == p->L1.ckpt || c < 0) return p->L1;
+  std::lock_guard<std::mutex> lk(p->lay_mu);
+  for (auto& L : p->lay_cache)
+    if (L->ckpt == c) return *L;
+  p->lay_cache.emplace_back(new Layout());
+  make_layout(*p, c, *p->lay_cache.back());
+  return *p->lay_cache.back();
+}
 
 }  // namespace
 
@@ -268,56 +348,11 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   }
   const int nl = (int)p->lv.size();
 
-  // ---- checkpoint choice: most fused fine levels subject to depth <= 8, smem, and >= 2 waves ----
+  // ---- checkpoint and workspace layout of single runs ----
   {
-    int best = -1;
-    for (int c = 0; c < nl; ++c) {
-      const int nf = nl - 1 - c;
-      if (nf > kMaxFine) continue;
-      if (fine_smem_bytes(*p, c, nullptr, nullptr, nullptr, nullptr, nullptr) > kFineSmemLimit) continue;
-      const int64_t nb = (p->lv[c].Ml + kBundle - 1) / kBundle;
-      if (best < 0) best = c;
-      if (nb >= 2 * 148) { best = c; break; }
-      best = c;  // keep moving finer while parallelism is insufficient
-    }
-    if (const char* env = std::getenv("RQMC_CKPT_W")) {  // tuning override: checkpoint at level w
-      const int wv = std::atoi(env);
-      for (int c = 0; c < nl; ++c)
-        if (p->lv[c].w == wv && nl - 1 - c <= kMaxFine &&
-            fine_smem_bytes(*p, c, nullptr, nullptr, nullptr, nullptr, nullptr) <= kFineSmemLimit)
-          best = c;
-    }
-    if (best < 0) { delete p; return bad(RQMC_EUNSUPPORTED, "no feasible checkpoint level"); }
-    p->ckpt = best;
-    p->nfine = nl - 1 - best;
-    for (int i = 0; i < nl; ++i) p->lv[i].coarse = i <= best;
-    p->nbundles = (p->lv[best].Ml + kBundle - 1) / kBundle;
-    p->fine_smem = fine_smem_bytes(*p, best, &p->fine_xs_off, &p->fine_as_off, &p->fine_as_stride,
-                                   &p->fine_acc_off, &p->leafruns);
-  }
-
-  // ---- workspace layout ----
-  {
-    size_t off = 0;
-    p->off_x = 0;
-    for (auto& L : p->lv) {
-      L.ldx = L.coarse ? (L.s_w + 1) / 2 * 2 : L.s_w;
-      L.xoff = (int64_t)(off / sizeof(double));
-      off = align_up(off + (size_t)L.Ml * L.ldx * sizeof(double), 256);
-      p->max_gen_entries = std::max<int64_t>(p->max_gen_entries, L.Ml * L.ldx);
-    }
-    p->ldr = (p->tau + 1) / 2 * 2;
-    size_t rsz[2] = {0, 0};
-    for (int i = 0; i <= p->ckpt; ++i) {
-      p->lv[i].rbuf = i & 1;
-      rsz[i & 1] = std::max(rsz[i & 1], (size_t)p->lv[i].Ml * p->ldr * sizeof(double));
-    }
-    p->off_r[0] = off; off = align_up(off + rsz[0], 256);
-    p->off_r[1] = off; off = align_up(off + rsz[1], 256);
-    p->off_part = off; off = align_up(off + (size_t)p->nbundles * sizeof(double), 256);
-    p->off_fsum = off; off = align_up(off + sizeof(double), 256);
-    p->off_a = off; off = align_up(off + (size_t)p->s * p->ldr * sizeof(double), 256);
-    p->total = off;
+    const int c = choose_ckpt(*p, 1);
+    if (c < 0) { delete p; return bad(RQMC_EUNSUPPORTED, "no feasible checkpoint level"); }
+    make_layout(*p, c, p->L1);
   }
   *out = p;
   return RQMC_OK;
@@ -336,11 +371,21 @@ void rqmc_plan_destroy(rqmc_plan_t p) {
 rqmc_status rqmc_plan_summary_get(rqmc_plan_t p, rqmc_plan_summary* o) {
   if (!p || !o) return RQMC_EINVAL;
   o->n_levels = (int)p->lv.size();
-  o->checkpoint = p->ckpt;
-  o->n_fine = p->nfine;
-  o->n_bundles = p->nbundles;
+  o->checkpoint = p->L1.ckpt;
+  o->n_fine = p->L1.nfine;
+  o->n_bundles = p->L1.nbundles;
   o->N_local = p->Nl;
   o->s_star = p->s_star;
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_plan_summary_batch(rqmc_plan_t p, int R, rqmc_plan_summary* o) {
+  if (!p || !o || R < 1) return RQMC_EINVAL;
+  if (rqmc_status s = rqmc_plan_summary_get(p, o)) return s;
+  const Layout& L = layout_for(p, R);
+  o->checkpoint = L.ckpt;
+  o->n_fine = L.nfine;
+  o->n_bundles = L.nbundles;
   return RQMC_OK;
 }
 
@@ -348,7 +393,7 @@ rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* o) {
   if (!p || !o || idx < 0 || idx >= (int)p->lv.size()) return RQMC_EINVAL;
   const Level& L = p->lv[idx];
   o->w = L.w; o->j_lo = L.j_lo; o->s_w = L.s_w; o->M = L.M; o->M_local = L.Ml;
-  o->parent = L.parent; o->coarse = L.coarse;
+  o->parent = L.parent; o->coarse = p->L1.lv[idx].coarse;
   return RQMC_OK;
 }
 
@@ -366,7 +411,7 @@ rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* rows, double* ma
 
 rqmc_status rqmc_workspace_size(rqmc_plan_t p, size_t* bytes) {
   if (!p || !bytes) return RQMC_EINVAL;
-  *bytes = p->total;
+  *bytes = p->L1.total;
   return RQMC_OK;
 }
 
@@ -392,16 +437,16 @@ rqmc_status upload(rqmc_plan_s* p) {
   return RQMC_OK;
 }
 
-GenArgs gen_args(const rqmc_plan_s* p, void* work) {
+GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
   GenArgs g{};
   g.kind = p->kind; g.map = p->map; g.b = p->b; g.m = p->m; g.shifted = p->shifted;
   g.rank = p->rank; g.world = p->world; g.nlev = (int)p->lv.size();
   g.zero_u = p->shifted ? std::ldexp(1.0, -53) : 0.5 / (double)p->N;
   g.seed = p->seed;
   g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds;
-  g.X = reinterpret_cast<double*>(static_cast<char*>(work) + p->off_x);
-  for (size_t i = 0; i < p->lv.size(); ++i) {
-    const Level& L = p->lv[i];
+  g.X = reinterpret_cast<double*>(static_cast<char*>(work) + lay.off_x);
+  for (size_t i = 0; i < lay.lv.size(); ++i) {
+    const Level& L = lay.lv[i];
     g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, 0, std::ldexp(1.0, -(p->m - L.w))};
   }
   return g;
@@ -422,7 +467,8 @@ struct RunRand {
   int srep;
 };
 
-rqmc_status run_core(rqmc_plan_s* p, int nrep, char* w, size_t rep_bytes, const RunRand& rr, const double* dA,
+rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_t rep_bytes, const RunRand& rr,
+                     const double* dA,
                      int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
                      cudaStream_t st) {
   const bool want_f = f != RQMC_F_NONE && d_fsum;
@@ -433,22 +479,22 @@ rqmc_status run_core(rqmc_plan_s* p, int nrep, char* w, size_t rep_bytes, const 
   mark(0);
 
   // a2: reduced points of every level (all replicas: grid.z)
-  GenArgs g = gen_args(p, w);
+  GenArgs g = gen_args(p, lay, w);
   g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
-  if (rqmc_status s = check_cuda(p, launch_gen(g, p->max_gen_entries, nrep, st), "k_gen")) return s;
+  if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
 
   // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine
-  for (int i = 0; i <= p->ckpt; ++i) {
-    const Level& L = p->lv[i];
+  for (int i = 0; i <= lay.ckpt; ++i) {
+    const Level& L = lay.lv[i];
     GemmArgs a{};
     a.X = g.X + L.xoff; a.ldx = L.ldx; a.M = L.Ml; a.K = L.s_w;
     a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda; a.tau = p->tau;
     if (L.parent >= 0) {
-      const Level& P = p->lv[L.parent];
-      a.Rp = reinterpret_cast<const double*>(w + p->off_r[P.rbuf]); a.ldp = p->ldr; a.Mp = P.Ml;
+      const Level& P = lay.lv[L.parent];
+      a.Rp = reinterpret_cast<const double*>(w + lay.off_r[P.rbuf]); a.ldp = lay.ldr; a.Mp = P.Ml;
     }
-    a.R = reinterpret_cast<double*>(w + p->off_r[L.rbuf]); a.ldr = p->ldr;
+    a.R = reinterpret_cast<double*>(w + lay.off_r[L.rbuf]); a.ldr = lay.ldr;
     a.xrep = rep_d; a.rrep = rep_d;
     if (rqmc_status s = check_cuda(p, launch_gemm(a, nrep, st), "k_level_gemm")) return s;
   }
@@ -457,16 +503,16 @@ rqmc_status run_core(rqmc_plan_s* p, int nrep, char* w, size_t rep_bytes, const 
 
   // a3+a4+a5 fine levels fused with f / Y store
   FineArgs fa{};
-  const Level& R = p->lv[p->ckpt];
-  fa.root = reinterpret_cast<const double*>(w + p->off_r[R.rbuf]); fa.ldroot = p->ldr; fa.Mroot = R.Ml;
-  fa.NF = p->nfine;
-  for (int i = 0; i < p->nfine; ++i) {
-    const Level& L = p->lv[p->ckpt + 1 + i];
+  const Level& R = lay.lv[lay.ckpt];
+  fa.root = reinterpret_cast<const double*>(w + lay.off_r[R.rbuf]); fa.ldroot = lay.ldr; fa.Mroot = R.Ml;
+  fa.NF = lay.nfine;
+  for (int i = 0; i < lay.nfine; ++i) {
+    const Level& L = lay.lv[lay.ckpt + 1 + i];
     FineLevel& F = fa.lv[i];
     F.X = g.X + L.xoff; F.ldx = L.ldx; F.K = L.s_w; F.j_lo = L.j_lo;
     F.runs = (int)(L.Ml / R.Ml);
     F.fan = i == 0 ? F.runs : F.runs / fa.lv[i - 1].runs;
-    F.xs_off = p->fine_xs_off[i]; F.as_off = p->fine_as_off[i];
+    F.xs_off = lay.fine_xs_off[i]; F.as_off = lay.fine_as_off[i];
   }
   fa.A = dA; fa.lda = lda; fa.tau = p->tau;
   fa.a_vec = ((uintptr_t)dA % 16 == 0) && (lda % 2 == 0) && (p->tau % 2 == 0);
@@ -475,17 +521,17 @@ rqmc_status run_core(rqmc_plan_s* p, int nrep, char* w, size_t rep_bytes, const 
   fa.fk = want_f ? (int)f : -1;
   fa.fp0 = fparam ? fparam[0] : 0.0;
   fa.fp1 = fparam ? fparam[1] : 0.0;
-  fa.partial = reinterpret_cast<double*>(w + p->off_part);
-  fa.leafruns = p->leafruns;
-  fa.as_stride = p->fine_as_stride;
-  fa.root_off = 2 * p->fine_as_stride;
-  fa.acc_off = p->fine_acc_off;
-  fa.smem_bytes = p->fine_smem;
+  fa.partial = reinterpret_cast<double*>(w + lay.off_part);
+  fa.leafruns = lay.leafruns;
+  fa.as_stride = lay.fine_as_stride;
+  fa.root_off = 2 * lay.fine_as_stride;
+  fa.acc_off = lay.fine_acc_off;
+  fa.smem_bytes = lay.fine_smem;
   fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
-  if (rqmc_status s = check_cuda(p, launch_fine(fa, p->nbundles, nrep, st), "k_fine")) return s;
+  if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st), "k_fine")) return s;
   mark(3);
   if (want_f)
-    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, p->nbundles, rep_d, nrep, d_fsum, st), "k_reduce"))
+    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, lay.nbundles, rep_d, nrep, d_fsum, st), "k_reduce"))
       return s;
   mark(4);
   return RQMC_OK;
@@ -500,21 +546,22 @@ rqmc_status check_f(rqmc_plan_s* p, rqmc_f f, const double* fparam) {
 rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
                 const double* fparam, double* d_fsum, void* dwork, size_t wbytes, cudaStream_t st) {
   if (!p || !dA || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
-  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->total));
+  if (wbytes < p->L1.total) return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->L1.total));
   if (lda < p->tau || (dY && ldy < p->tau)) return fail(p, RQMC_EDIM, "lda/ldy < tau");
   if (rqmc_status s = check_f(p, f, fparam)) return s;
   const bool want_f = f != RQMC_F_NONE && d_fsum;
   if (!want_f && !dY) return RQMC_OK;
   if (rqmc_status s = upload(p)) return s;
   const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
-  return run_core(p, 1, static_cast<char*>(dwork), p->off_fsum, rr, dA, lda, dY, ldy, f, fparam, d_fsum, st);
+  return run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, dA, lda, dY, ldy, f, fparam, d_fsum,
+                  st);
 }
 
 // bytes of one replica's workspace slice [X^red][R0][R1][partials] and of a chunk of n replicas
-size_t rep_slice_bytes(const rqmc_plan_s* p) { return p->off_fsum; }
-size_t batch_bytes(const rqmc_plan_s* p, int64_t n) {
+size_t rep_slice_bytes(const Layout& lay) { return lay.off_fsum; }
+size_t batch_bytes(const rqmc_plan_s* p, const Layout& lay, int64_t n) {
   const size_t tab = (p->kind == RQMC_REDUCED_MC ? 1 : (size_t)p->s) * sizeof(double);
-  return (size_t)n * rep_slice_bytes(p) + align_up((size_t)n * tab, 256);
+  return (size_t)n * rep_slice_bytes(lay) + align_up((size_t)n * tab, 256);
 }
 
 }  // namespace
@@ -535,16 +582,16 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream) {
   if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
-  if (wbytes < p->total) return fail(p, RQMC_EINVAL, "workspace too small");
+  if (wbytes < p->L1.total) return fail(p, RQMC_EINVAL, "workspace too small");
   if (lda < p->tau) return fail(p, RQMC_EDIM, "lda < tau");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(dwork);
-  double* dA = reinterpret_cast<double*>(w + p->off_a);
-  double* dsum = reinterpret_cast<double*>(w + p->off_fsum);
-  cudaError_t e = cudaMemcpy2DAsync(dA, (size_t)p->ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
+  double* dA = reinterpret_cast<double*>(w + p->L1.off_a);
+  double* dsum = reinterpret_cast<double*>(w + p->L1.off_fsum);
+  cudaError_t e = cudaMemcpy2DAsync(dA, (size_t)p->L1.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
                                     (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, st);
   if (rqmc_status s = check_cuda(p, e, "H2D A")) return s;
-  if (rqmc_status s = rqmc_qn(p, dA, p->ldr, f, fparam, dsum, dwork, wbytes, stream)) return s;
+  if (rqmc_status s = rqmc_qn(p, dA, p->L1.ldr, f, fparam, dsum, dwork, wbytes, stream)) return s;
   e = cudaMemcpyAsync(h_fsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   return check_cuda(p, e, "D2H fsum");
@@ -552,7 +599,7 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
 
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes) {
   if (!p || !bytes || R < 1) return RQMC_EINVAL;
-  *bytes = batch_bytes(p, R);
+  *bytes = batch_bytes(p, layout_for(p, R), R);
   return RQMC_OK;
 }
 
@@ -582,16 +629,30 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
     tab = hseeds;
     per = sizeof(uint64_t);
   }
+  // layout for the replicas that run together; a smaller workspace means smaller chunks, which
+  // may in turn want a finer checkpoint (re-evaluated until stable)
+  const Layout* lay = &layout_for(p, R);
   int64_t chunk = R;
-  while (chunk > 0 && batch_bytes(p, chunk) > wbytes) --chunk;
+  for (int it = 0; it < 4; ++it) {
+    chunk = R;
+    while (chunk > 0 && batch_bytes(p, *lay, chunk) > wbytes) --chunk;
+    if (chunk == 0) break;
+    const Layout* l2 = &layout_for(p, chunk);
+    if (l2 == lay) break;
+    lay = l2;
+  }
+  if (chunk == 0) {
+    lay = &p->L1;
+    chunk = wbytes >= batch_bytes(p, *lay, 1) ? 1 : 0;
+  }
   if (chunk == 0) return fail(p, RQMC_EINVAL, "workspace too small for one replica: need " +
-                                                  std::to_string(batch_bytes(p, 1)));
+                                                  std::to_string(batch_bytes(p, p->L1, 1)));
   if (rqmc_status s = upload(p)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(dwork);
   for (int64_t r0 = 0; r0 < R; r0 += chunk) {
     const int n = (int)std::min<int64_t>(chunk, R - r0);
-    char* dtab = w + (size_t)chunk * rep_slice_bytes(p);
+    char* dtab = w + (size_t)chunk * rep_slice_bytes(*lay);
     cudaError_t e = cudaMemcpyAsync(dtab, static_cast<const char*>(tab) + (size_t)r0 * per, (size_t)n * per,
                                     cudaMemcpyHostToDevice, st);
     if (rqmc_status s = check_cuda(p, e, "H2D batch shifts")) return s;
@@ -599,7 +660,7 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
     if (p->kind == RQMC_LATTICE) rr.shift = reinterpret_cast<const double*>(dtab);
     else if (p->kind == RQMC_DIGITAL_NET) rr.dshift = reinterpret_cast<const uint64_t*>(dtab);
     else rr.seeds = reinterpret_cast<const uint64_t*>(dtab);
-    if (rqmc_status s = run_core(p, n, w, rep_slice_bytes(p), rr, dA, lda, nullptr, 0, f, fparam, d_fsum + r0, st))
+    if (rqmc_status s = run_core(p, *lay, n, w, rep_slice_bytes(*lay), rr, dA, lda, nullptr, 0, f, fparam, d_fsum + r0, st))
       return s;
   }
   return RQMC_OK;
@@ -610,7 +671,7 @@ rqmc_status rqmc_points(rqmc_plan_t p, int idx, int64_t r0, int64_t count, uint6
   if (!p || idx < 0 || idx >= (int)p->lv.size() || r0 < 0 || count < 0 || r0 + count > p->lv[idx].Ml)
     return fail(p, RQMC_EINVAL, "bad level / row range");
   if (rqmc_status s = upload(p)) return s;
-  GenArgs g = gen_args(p, nullptr);
+  GenArgs g = gen_args(p, p->L1, nullptr);
   return check_cuda(p, launch_points(g, idx, r0, count, d_words, d_vals, static_cast<cudaStream_t>(stream)),
                     "k_points");
 }

@@ -1,8 +1,9 @@
 """Batched randomisation: R independent shifts
 (lattice), digital shifts (net) or seeds (reduced MC) of one plan and one A, run together.
 
-Bars: replica r is BIT-IDENTICAL to a plain rqmc_qn run of a plan holding that randomisation (same
-kernels, same summation order), and within relative 1e-12 of the oracle's Q_N sum.
+Bars: replica r is BIT-IDENTICAL to a plain rqmc_qn run of a plan holding that randomisation when the
+batch uses the single-run layout (same checkpoint); with a deeper batch checkpoint (replicas add
+parallelism) it agrees to the oracle tolerance; always within relative 1e-12 of the oracle's Q_N sum.
 """
 import numpy as np
 import pytest
@@ -45,23 +46,32 @@ def test_batch_equals_single_runs_and_oracle(rq, seed, b, m, s, tau, kind, mappi
     A = dev(prob.A)
     pl = rq.Plan.from_problem(prob)
     sums = pl.qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
+    same_layout = pl.summary_batch(R)["checkpoint"] == pl.summary()["checkpoint"]
     for r in range(R):
         pr = _with(prob, kw, r)
         single = float(rq.Plan.from_problem(pr).qn_sum(A, prob.f, prob.fparam).item())
-        assert sums[r] == single, (r, sums[r], single)
         fo = oracle.f_rows(pr, np.arange(pr.N))
+        if same_layout:
+            assert sums[r] == single, (r, sums[r], single)
+        else:
+            assert abs(sums[r] - single) <= 1e-12 * np.abs(fo).sum()
         assert abs(sums[r] - oracle.neumaier(fo)) <= 1e-12 * np.abs(fo).sum()
 
 
-def test_batch_chunking_identical(rq):
-    """A workspace for 2 replicas processes R = 7 in chunks; results identical to one launch of 7."""
+def test_batch_chunking(rq):
+    """A workspace for 2 replicas processes R = 7 in chunks; equal to one launch of 7 (bit-identical
+    when both use the same layout, else to rounding)."""
     prob = W.make_random(9, 2, 12, 80, 50, shifted=True, mapping=W.MAP_INVNORM)
     kw = _replicas(prob, 7, 9)
     A = dev(prob.A)
-    full = rq.Plan.from_problem(prob).qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
+    pl7 = rq.Plan.from_problem(prob)
+    full = pl7.qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
     pl = rq.Plan.from_problem(prob)
     small = pl.qn_batch(A, prob.f, prob.fparam, max_workspace_bytes=pl.workspace_size_batch(2), **kw).cpu().numpy()
-    assert np.array_equal(full, small)
+    if pl7.summary_batch(7)["checkpoint"] == pl.summary_batch(2)["checkpoint"]:
+        assert np.array_equal(full, small)
+    else:
+        np.testing.assert_allclose(small, full, rtol=1e-12)
 
 
 def test_batch_c2_rqmc_estimate(rq):
@@ -72,9 +82,12 @@ def test_batch_c2_rqmc_estimate(rq):
     A = dev(prob.A)
     pl = rq.Plan.from_problem(prob)
     mean, se, q = pl.rqmc_estimate(A, prob.f, prob.fparam, **kw)
+    assert pl.summary_batch(16)["n_fine"] > pl.summary()["n_fine"]   # replicas let the batch fuse deeper
     for r in (0, 7, 15):
         single = float(rq.Plan.from_problem(_with(prob, kw, r)).qn_sum(A, prob.f, prob.fparam).item())
-        assert q[r] == single / prob.N
+        assert abs(q[r] - single / prob.N) <= 1e-12 * abs(q[r])
+    # the batch layout's sums agree with the oracle (full naive Q_N of one replica)
+    assert abs(q[3] * prob.N - oracle.qn_sum(_with(prob, kw, 3))) <= 1e-12 * abs(q[3] * prob.N)
     assert mean == pytest.approx(np.mean(q), rel=1e-15) and se > 0 and se < 0.1 * abs(mean)
 
 
