@@ -285,7 +285,7 @@ def main():
     # ---- roofline of the dominant kernel (k_fine: fused fine levels on the fp64 DFMA pipe)
     levels = plan.levels()
     if R > 1:
-        summ = plan.summary_batch(R)
+        summ = plan.summary_batch(R, prob.f)
     ck = summ["checkpoint"]
     fine_flops = R * 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[ck + 1:])
     coarse_flops = R * 2.0 * prob.tau * sum(L["M_local"] * L["s_w"] for L in levels[:ck + 1])

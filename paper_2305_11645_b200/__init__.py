@@ -99,7 +99,7 @@ def lib():
         L.rqmc_points.argtypes = [vp, C.c_int, i64, i64, vp, vp, vp]
         L.rqmc_profile_enable.argtypes = [vp, C.c_int]
         L.rqmc_workspace_size_batch.argtypes = [vp, C.c_int, C.POINTER(C.c_size_t)]
-        L.rqmc_plan_summary_batch.argtypes = [vp, C.c_int, C.POINTER(Summary)]
+        L.rqmc_plan_summary_batch.argtypes = [vp, C.c_int, C.c_int, C.POINTER(Summary)]
         L.rqmc_qn_batch.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), vp, i64,
                                     C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_profile_read.argtypes = [vp, C.POINTER(C.c_int), dp, dp, dp, dp]
@@ -237,10 +237,11 @@ class Plan:
             dist.all_reduce(part, group=group)
         return float(part.item()) / self.N
 
-    def summary_batch(self, R: int) -> dict:
-        """Summary of the layout a batch of R replicas runs with (checkpoint may differ from summary())."""
+    def summary_batch(self, R: int, f: int = F_MEAN) -> dict:
+        """Summary of the layout a batch of R replicas with integrand f runs with (checkpoint may differ
+        from summary())."""
         o = Summary()
-        self._check(lib().rqmc_plan_summary_batch(self._h, R, C.byref(o)))
+        self._check(lib().rqmc_plan_summary_batch(self._h, R, f, C.byref(o)))
         return o.as_dict()
 
     def workspace_size_batch(self, R: int) -> int:

@@ -146,7 +146,8 @@ int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
     if (nb * reps >= 2 * 148) { best = c; break; }
     best = c;  // keep moving finer while parallelism is insufficient
   }
-  if (const char* env = std::getenv("RQMC_CKPT_W")) {  // tuning override: checkpoint at level w
+  const char* env = std::getenv("RQMC_CKPT_W");        // tuning override: checkpoint at level w
+  if (env && *env) {
     const int wv = std::atoi(env);
     for (int c = 0; c < nl; ++c)
       if (p.lv[c].w == wv && nl - 1 - c <= kMaxFine &&
@@ -191,8 +192,11 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
 }
 
 // Layout for a batch of `reps` concurrent replicas (cached; the single-run layout when equal).
-const Layout& layout_for(rqmc_plan_s* p, int64_t reps) {
-  const int c = choose_ckpt(*p, reps);
+// g = exp (RQMC_F_CALL_MEAN_EXP) keeps the single-run checkpoint: its fused fine kernel is bound by
+// the N tau exp evaluations and register pressure, and measured slower fused deeper (C2, R = 64:
+// 4.51 ms at checkpoint w = 6 vs 3.98 ms at w = 2).
+const Layout& layout_for(rqmc_plan_s* p, int64_t reps, int f) {
+  const int c = choose_ckpt(*p, f == RQMC_F_CALL_MEAN_EXP ? 1 : reps);
   if (c == p->L1.ckpt || c < 0) return p->L1;
   std::lock_guard<std::mutex> lk(p->lay_mu);
   for (auto& L : p->lay_cache)
@@ -379,10 +383,10 @@ rqmc_status rqmc_plan_summary_get(rqmc_plan_t p, rqmc_plan_summary* o) {
   return RQMC_OK;
 }
 
-rqmc_status rqmc_plan_summary_batch(rqmc_plan_t p, int R, rqmc_plan_summary* o) {
+rqmc_status rqmc_plan_summary_batch(rqmc_plan_t p, int R, int f, rqmc_plan_summary* o) {
   if (!p || !o || R < 1) return RQMC_EINVAL;
   if (rqmc_status s = rqmc_plan_summary_get(p, o)) return s;
-  const Layout& L = layout_for(p, R);
+  const Layout& L = layout_for(p, R, f);
   o->checkpoint = L.ckpt;
   o->n_fine = L.nfine;
   o->n_bundles = L.nbundles;
@@ -599,7 +603,8 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
 
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes) {
   if (!p || !bytes || R < 1) return RQMC_EINVAL;
-  *bytes = batch_bytes(p, layout_for(p, R), R);
+  // enough for either layout a batch of R may use (the choice depends on f)
+  *bytes = std::max(batch_bytes(p, layout_for(p, R, RQMC_F_MEAN), R), batch_bytes(p, p->L1, R));
   return RQMC_OK;
 }
 
@@ -631,13 +636,13 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
   }
   // layout for the replicas that run together; a smaller workspace means smaller chunks, which
   // may in turn want a finer checkpoint (re-evaluated until stable)
-  const Layout* lay = &layout_for(p, R);
+  const Layout* lay = &layout_for(p, R, f);
   int64_t chunk = R;
   for (int it = 0; it < 4; ++it) {
     chunk = R;
     while (chunk > 0 && batch_bytes(p, *lay, chunk) > wbytes) --chunk;
     if (chunk == 0) break;
-    const Layout* l2 = &layout_for(p, chunk);
+    const Layout* l2 = &layout_for(p, chunk, f);
     if (l2 == lay) break;
     lay = l2;
   }

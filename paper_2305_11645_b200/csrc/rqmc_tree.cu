@@ -243,20 +243,27 @@ struct TreeRun {
   // leaves 2 tg, 2 tg + 1 (NQ = 2; leaf tg for NQ = 1), accumulated in registers.
   template <int P>
   __device__ __forceinline__ void bottom_b2(const double (&Sp)[NV], int jp) {
+    bottom_nodes<P, 0, NQ>(Sp, jp);
+  }
+
+  // NN K = 4 nodes starting at node N0 of the bottom block; lane tg ends with the column-slice sums of
+  // NN of the 4 NN leaves, accumulated into racc[P RW + N0 + i], i < NN
+  template <int P, int N0, int NN>
+  __device__ __forceinline__ void bottom_nodes(const double (&Sp)[NV], int jp) {
     constexpr int I1 = NF - 2, I0 = NF - 1;
     constexpr int RP2 = (I2 == 0) ? 1 : T::runs(I2) / 2, RP1 = T::runs(I1) / 2, RP0 = T::runs(I0) / 2;
-    constexpr int NL = 4 * NQ;
+    constexpr int NL = 4 * NN;
     int jl[NL];
     double v[NL];
 #pragma unroll
-    for (int n = 0; n < NQ; ++n) {
-      const int q2 = (I2 == 0) ? c.grp : n;
+    for (int n = 0; n < NN; ++n) {
+      const int q2 = (I2 == 0) ? c.grp : N0 + n;
       const int j2 = jp + q2 * RP2;
 #pragma unroll
       for (int l = 0; l < 4; ++l) jl[4 * n + l] = j2 + (l >> 1) * RP1 + (l & 1) * RP0;
     }
 #pragma unroll
-    for (int n = 0; n < NQ; ++n) {
+    for (int n = 0; n < NN; ++n) {
       const int j2 = jl[4 * n];
       double S2[NV];
       tree_step<4, NFR>(xs(I2, j2), as(I2), c, Sp, S2);
@@ -290,7 +297,7 @@ struct TreeRun {
       for (int i = 0; i < NL / 4; ++i) {
         const double keep = hi0 ? u[i + NL / 4] : u[i];
         const double send = hi0 ? u[i] : u[i + NL / 4];
-        racc[P * RW + i] += keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        racc[P * RW + N0 + i] += keep + __shfl_xor_sync(0xffffffffu, send, 1);
       }
     }
   }

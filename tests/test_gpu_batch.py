@@ -46,7 +46,7 @@ def test_batch_equals_single_runs_and_oracle(rq, seed, b, m, s, tau, kind, mappi
     A = dev(prob.A)
     pl = rq.Plan.from_problem(prob)
     sums = pl.qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
-    same_layout = pl.summary_batch(R)["checkpoint"] == pl.summary()["checkpoint"]
+    same_layout = pl.summary_batch(R, prob.f)["checkpoint"] == pl.summary()["checkpoint"]
     for r in range(R):
         pr = _with(prob, kw, r)
         single = float(rq.Plan.from_problem(pr).qn_sum(A, prob.f, prob.fparam).item())
@@ -68,7 +68,7 @@ def test_batch_chunking(rq):
     full = pl7.qn_batch(A, prob.f, prob.fparam, **kw).cpu().numpy()
     pl = rq.Plan.from_problem(prob)
     small = pl.qn_batch(A, prob.f, prob.fparam, max_workspace_bytes=pl.workspace_size_batch(2), **kw).cpu().numpy()
-    if pl7.summary_batch(7)["checkpoint"] == pl.summary_batch(2)["checkpoint"]:
+    if pl7.summary_batch(7, prob.f)["checkpoint"] == pl.summary_batch(2, prob.f)["checkpoint"]:
         assert np.array_equal(full, small)
     else:
         np.testing.assert_allclose(small, full, rtol=1e-12)
@@ -82,7 +82,8 @@ def test_batch_c2_rqmc_estimate(rq):
     A = dev(prob.A)
     pl = rq.Plan.from_problem(prob)
     mean, se, q = pl.rqmc_estimate(A, prob.f, prob.fparam, **kw)
-    assert pl.summary_batch(16)["n_fine"] > pl.summary()["n_fine"]   # replicas let the batch fuse deeper
+    assert pl.summary_batch(16, prob.f)["n_fine"] == pl.summary()["n_fine"]   # g = exp: no deeper fusion
+    assert pl.summary_batch(16, W.F_EXP_MEAN)["n_fine"] > pl.summary()["n_fine"]   # cheap g: deeper
     for r in (0, 7, 15):
         single = float(rq.Plan.from_problem(_with(prob, kw, r)).qn_sum(A, prob.f, prob.fparam).item())
         assert abs(q[r] - single / prob.N) <= 1e-12 * abs(q[r])
