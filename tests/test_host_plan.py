@@ -165,3 +165,32 @@ def test_gloo_world2_partition_allreduce(rq):
     prob = W.make_random(77, 2, 9, 40, 6, shifted=True, mapping=W.MAP_INVNORM)
     full = oracle.qn_sum(prob) / prob.N
     assert abs(res[0] - full) <= 1e-13 * abs(full) and res[0] == res[1]
+
+
+# ------------------------------------------------------------------ reduced MC and batch layouts (host)
+
+def test_reduced_mc_plan(rq):
+    """Reduced MC: no generating vector; shifts rejected; coordinates with w_j >= m keep
+    one i.i.d. draw each (N_j = 1: a 1-row level m, P:981 N_{s+1} = 1)."""
+    p = rq.Plan(2, 4, 5, 3, [0, 1, 1, 4, 6], kind=rq.REDUCED_MC, seed=5)
+    lv = p.levels()
+    assert [L["w"] for L in lv] == [4, 1, 0] and [L["s_w"] for L in lv] == [2, 2, 1]
+    assert lv[0]["M"] == 1
+    with pytest.raises(rq.RqmcError) as ei:
+        rq.Plan(2, 4, 3, 3, [0, 1, 1], kind=rq.REDUCED_MC, shift=[0.1, 0.2, 0.3])
+    assert ei.value.name == "ESHIFT"
+
+
+def test_batch_layout_and_workspace(rq):
+    """replicas add parallelism, so a batch may fuse more fine levels than a
+    single run (cheap g); g = exp keeps the single-run checkpoint; the batch workspace covers R
+    replica slices."""
+    prob = W.make_config("C2")
+    pl = rq.Plan.from_problem(prob)
+    one = pl.summary()
+    deep = pl.summary_batch(64, W.F_EXP_MEAN)
+    assert deep["n_fine"] > one["n_fine"] and deep["n_bundles"] * 64 >= 2 * 148
+    assert pl.summary_batch(64, W.F_CALL_MEAN_EXP)["checkpoint"] == one["checkpoint"]
+    assert pl.summary_batch(1, W.F_EXP_MEAN)["checkpoint"] == one["checkpoint"]
+    assert pl.workspace_size_batch(16) >= 16 * pl.workspace_size_batch(1) // 2
+    assert pl.workspace_size_batch(16) > pl.workspace_size_batch(1)
