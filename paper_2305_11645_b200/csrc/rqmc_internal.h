@@ -20,7 +20,7 @@ struct GenLevel {
   int64_t M;      // global distinct rows b^{m-w}
   int64_t Ml;     // local rows
   int64_t xoff;   // offset (doubles) of X^red in the workspace
-  int j_lo, s_w, ldx, pad;
+  int j_lo, s_w, ldx, tc_log;   // tc_log: log2 of the generator's column-tile width min(32, pow2 >= ldx)
   double inv_M;   // 2^-(m-w) for b = 2 (exact scaling of t / M)
 };
 

@@ -451,7 +451,9 @@ GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
   g.X = reinterpret_cast<double*>(static_cast<char*>(work) + lay.off_x);
   for (size_t i = 0; i < lay.lv.size(); ++i) {
     const Level& L = lay.lv[i];
-    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, 0, std::ldexp(1.0, -(p->m - L.w))};
+    int tcl = 0;
+    while (tcl < 5 && (1 << tcl) < L.ldx) ++tcl;
+    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, tcl, std::ldexp(1.0, -(p->m - L.w))};
   }
   return g;
 }
