@@ -512,11 +512,12 @@ static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, int nrep, cudaSt
   return launch_fine_t<NF, BotNone>(a, nb, nrep, st);
 }
 
-cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st);
+cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts);
 
-cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
+cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
+  *nparts = nb;
   if (std::getenv("RQMC_NO_TREE") == nullptr) {
-    const cudaError_t e = launch_tree(a, nb, nrep, st);
+    const cudaError_t e = launch_tree(a, nb, nrep, st, nparts);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (a.NF) {

@@ -25,24 +25,33 @@ namespace rqmc {
 #ifndef RQMC_GEMM_STAGES
 #define RQMC_GEMM_STAGES 2
 #endif
+#ifndef RQMC_GEMM_PARENT_LAST
+#define RQMC_GEMM_PARENT_LAST 0
+#endif
 #ifndef RQMC_GEMM_SIBLING
 #define RQMC_GEMM_SIBLING 1
 #endif
-constexpr int kGemmBN = 64, kGemmBK = 16, kGemmStages = RQMC_GEMM_STAGES;
+#ifndef RQMC_GEMM_BK
+#define RQMC_GEMM_BK 16
+#endif
+constexpr int kGemmBN = 64, kGemmBK = RQMC_GEMM_BK, kGemmStages = RQMC_GEMM_STAGES;
 
 template <int BM>
 constexpr int gemm_smem_bytes() {
   return (int)sizeof(double) * kGemmStages * (BM * (kGemmBK + 4) + kGemmBK * (kGemmBN + 4));
 }
 
-template <int BM, int CH>
-__global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu, int64_t y0) {
-  constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4, NT = BM * 2;
+// WMF = DMMA fragments per warp along M (warp tile 8 WMF x 32); warps (BM / 8 WMF) x 2
+template <int BM, int CH, int WMF>
+__global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
+                                                                   int64_t y0) {
+  constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4;
+  constexpr int NT = BM / (8 * WMF) * 64, WR = 8 * WMF;
   extern __shared__ __align__(16) double gsm[];
   double (*Xs)[BM][XS] = reinterpret_cast<double (*)[BM][XS]>(gsm);
   double (*As)[BK][AS] = reinterpret_cast<double (*)[BK][AS]>(gsm + NST * BM * XS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, tg = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, tg = lane & 3;  // warp grid (BM / WR) x 2
   // sibling-first row blocks: rows [rb, rb + BM) of slice u, valid while inside the slice and < M
   const int64_t yb = y0 + blockIdx.y;  // grid.y <= 65535: long levels launch in chunks
   const int64_t pb = yb / nu, u = yb - pb * nu;
@@ -74,6 +83,15 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
     }
   };
 
+  if (RQMC_GEMM_PARENT_LAST && Rpg) {  // warm L2 with the parent tile; it is added after the k-loop
+    for (int c = tid; c < BM * 4; c += NT) {
+      const int64_t row = r0 + c / 4;
+      if (row < rlim) {
+        const double* p = Rpg + (row % a.Mp) * a.ldp + c0 + (c % 4) * 16;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      }
+    }
+  }
   const int nk = (a.K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < NST - 1; ++s) {
@@ -81,16 +99,16 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
     cp_async_commit();
   }
 
-  double acc[4][4][2];
+  double acc[WMF][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = r0 + wm * 32 + i * 8 + g;
+  for (int i = 0; i < WMF; ++i) {
+    const int64_t row = r0 + wm * WR + i * 8 + g;
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
       acc[i][jn][0] = 0.0;
       acc[i][jn][1] = 0.0;
-      if (Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
+      if (!RQMC_GEMM_PARENT_LAST && Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
         const double* p = Rpg + (row % a.Mp) * a.ldp + col;
         if (CH == 2 && col + 1 < a.tau) {
           const double2 v = *reinterpret_cast<const double2*>(p);
@@ -112,13 +130,13 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
     const int buf = kt % NST;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[WMF], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = Xs[buf][wm * 32 + i * 8 + g][kk + tg];
+      for (int i = 0; i < WMF; ++i) af[i] = Xs[buf][wm * WR + i * 8 + g][kk + tg];
 #pragma unroll
       for (int jn = 0; jn < 4; ++jn) bf[jn] = As[buf][kk + tg][wn * 32 + jn * 8 + g];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WMF; ++i)
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
     }
@@ -126,9 +144,22 @@ __global__ void __launch_bounds__(BM * 2) k_level_gemm(const GemmArgs a, int64_t
   cp_async_wait<0>();
 
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = r0 + wm * 32 + i * 8 + g;
+  for (int i = 0; i < WMF; ++i) {
+    const int64_t row = r0 + wm * WR + i * 8 + g;
     if (row >= rlim) continue;
+    if (RQMC_GEMM_PARENT_LAST && Rpg) {
+#pragma unroll
+      for (int jn = 0; jn < 4; ++jn) {
+        const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
+        const double* p = Rpg + (row % a.Mp) * a.ldp + col;
+        if (col + 1 < a.tau) {
+          acc[i][jn][0] += p[0];
+          acc[i][jn][1] += p[1];
+        } else if (col < a.tau) {
+          acc[i][jn][0] += p[0];
+        }
+      }
+    }
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
@@ -146,7 +177,11 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
   if (a.M == 0 || nrep == 0) return cudaSuccess;
   const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
                    (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
-  const int BM = a.M >= 64 * 148 ? 128 : 64;
+#ifndef RQMC_GEMM_BM
+  const int BM = 64;   // 4 CTAs per SM: measured best on every C5 level (13.5 vs 14.1 ms, BM = 128 for long levels)
+#else
+  const int BM = RQMC_GEMM_BM;
+#endif
   // sibling-first ordering when the parent has at least one full row block; else plain row blocks
   int64_t mp_blk = a.M, nu = 1;
   if (RQMC_GEMM_SIBLING && a.Rp && a.Mp >= BM && a.Mp < a.M) {
@@ -155,6 +190,10 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
   const int sm = BM == 128 ? gemm_smem_bytes<128>() : gemm_smem_bytes<64>();
+#ifndef RQMC_GEMM_WMF
+#define RQMC_GEMM_WMF 4
+#endif
+  constexpr int WMF = RQMC_GEMM_WMF;
   auto go = [&](auto kern, int nt) -> cudaError_t {
     cudaError_t e = set_smem_once(kern, sm);
     if (e != cudaSuccess) return e;
@@ -166,8 +205,9 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
     }
     return cudaGetLastError();
   };
-  if (BM == 128) return vec ? go(k_level_gemm<128, 2>, 256) : go(k_level_gemm<128, 1>, 256);
-  return vec ? go(k_level_gemm<64, 2>, 128) : go(k_level_gemm<64, 1>, 128);
+  if (BM == 128)
+    return vec ? go(k_level_gemm<128, 2, WMF>, 128 / (8 * WMF) * 64) : go(k_level_gemm<128, 1, WMF>, 128 / (8 * WMF) * 64);
+  return vec ? go(k_level_gemm<64, 2, WMF>, 64 / (8 * WMF) * 64) : go(k_level_gemm<64, 1, WMF>, 64 / (8 * WMF) * 64);
 }
 
 }  // namespace rqmc

@@ -185,7 +185,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   }
   L.off_r[0] = off; off = align_up(off + rsz[0], 256);
   L.off_r[1] = off; off = align_up(off + rsz[1], 256);
-  L.off_part = off; off = align_up(off + (size_t)L.nbundles * sizeof(double), 256);
+  L.off_part = off; off = align_up(off + (size_t)2 * L.nbundles * sizeof(double), 256);  // see launch_fine
   L.off_fsum = off; off = align_up(off + sizeof(double), 256);
   L.off_a = off; off = align_up(off + (size_t)p.s * L.ldr * sizeof(double), 256);
   L.total = off;
@@ -534,10 +534,11 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   fa.acc_off = lay.fine_acc_off;
   fa.smem_bytes = lay.fine_smem;
   fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
-  if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st), "k_fine")) return s;
+  int64_t nparts = 0;
+  if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st, &nparts), "k_fine")) return s;
   mark(3);
   if (want_f)
-    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, lay.nbundles, rep_d, nrep, d_fsum, st), "k_reduce"))
+    if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, nparts, rep_d, nrep, d_fsum, st), "k_reduce"))
       return s;
   mark(4);
   return RQMC_OK;

@@ -35,11 +35,14 @@ namespace rqmc {
 // Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36
 // doubles (bank-conflict-free fragment loads); columns >= tau are zero in the A slab and root tile.
 // ------------------------------------------------------------------------------------------
+#ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
+#define RQMC_TREE_BUNDLE 16
+#endif
 #ifndef RQMC_TREE_NFR
 #define RQMC_TREE_NFR 4
 #endif
 
-template <int NF, int B, int NFR>
+template <int NF, int B, int NFR, int BUN>
 struct Tree {
   __host__ __device__ static constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
   __host__ __device__ static constexpr int K(int i) { return (B - 1) * ipow(B, NF - 1 - i); }  // s_w, w = NF-1-i
@@ -47,17 +50,19 @@ struct Tree {
   __host__ __device__ static constexpr int jlo(int i) { return ipow(B, NF - 1 - i) - 1; }      // first A row
   static constexpr int J = ipow(B, NF) - 1;                        // fine A rows
   static constexpr int CH = 4 / NFR;                               // column slices per group
-  static constexpr int WARPS = 8 * CH;
+  static constexpr int RWN = BUN / 8;                              // row warps (8 residues each)
+  static constexpr int WARPS = 2 * CH * RWN;
+  static constexpr int XP = BUN == 16 ? 20 : kPad;                 // X^red t-stride (conflict-free)
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int NV = 2 * NFR;                               // doubles per lane per node
   static constexpr int LEAVES = ipow(B, NF);
   static constexpr bool kRegAcc = (B == 2 && NF >= 3);             // register row sums (b = 2 bottom)
   static constexpr int ABUF = J * kPad;                            // one A slab
   static constexpr int ROOT = 2 * ABUF;                            // root tiles
-  static constexpr int XS = ROOT + 2 * kBundle * kPad;             // X subtree
-  static constexpr int XL = (B - 1) * ipow(B, NF) * kPad;          // X per level
+  static constexpr int XS = ROOT + 2 * BUN * kPad;                 // X subtree
+  static constexpr int XL = (B - 1) * ipow(B, NF) * XP;            // X per level
   static constexpr int ACC = XS + NF * XL;                         // rowacc [ch][leaf][t]
-  static constexpr int ACCN = kRegAcc ? 0 : CH * LEAVES * kBundle;
+  static constexpr int ACCN = kRegAcc ? 0 : CH * LEAVES * BUN;
   static constexpr int SMEM = (ACC + ACCN) * 8;
 };
 
@@ -68,14 +73,14 @@ struct TreeCtx {
 };
 
 // S = Sp + X^red[run] A_w, compile-time K (DMMA k-steps of 4, DFMA remainder); xs, as: level bases.
-template <int K, int NFR>
+template <int K, int NFR, int XP>
 __device__ __forceinline__ void tree_step(const double* xs, const double* as, const TreeCtx& c,
                                           const double (&Sp)[2 * NFR], double (&S)[2 * NFR]) {
   static_assert(K >= 1, "");
   if constexpr (K >= 4) {
     constexpr int NS = K / 4;
     const double* ab = as + c.cw + c.g;
-    double af = xs[c.tg * kPad], bf[NFR];
+    double af = xs[c.tg * XP], bf[NFR];
 #pragma unroll
     for (int cf = 0; cf < NFR; ++cf) bf[cf] = ab[c.tg * kPad + cf * 8];
 #pragma unroll
@@ -84,7 +89,7 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
 #pragma unroll
       for (int cf = 0; cf < NFR; ++cf) bfn[cf] = 0.0;
       if (s + 1 < NS) {
-        afn = xs[(4 * (s + 1) + c.tg) * kPad];
+        afn = xs[(4 * (s + 1) + c.tg) * XP];
 #pragma unroll
         for (int cf = 0; cf < NFR; ++cf) bfn[cf] = ab[(4 * (s + 1) + c.tg) * kPad + cf * 8];
       }
@@ -100,7 +105,7 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
   }
 #pragma unroll
   for (int kk = (K / 4) * 4; kk < K; ++kk) {
-    const double x = xs[kk * kPad];
+    const double x = xs[kk * XP];
 #pragma unroll
     for (int cf = 0; cf < NFR; ++cf) {
       const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + c.cw + cf * 8 + 2 * c.tg);
@@ -155,9 +160,9 @@ __device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[
   }
 }
 
-template <int NF, int B, int G, bool STY, int NFR>
+template <int NF, int B, int G, bool STY, int NFR, int BUN>
 struct TreeRun {
-  using T = Tree<NF, B, NFR>;
+  using T = Tree<NF, B, NFR, BUN>;
   static constexpr int NV = T::NV;
   static constexpr bool kB2 = (B == 2 && NF >= 3);
   static constexpr bool kRegAcc = T::kRegAcc && G > 0;
@@ -180,30 +185,30 @@ struct TreeRun {
   }
 
   __device__ __forceinline__ const double* xs(int i, int j) const {
-    return fsm + T::XS + i * T::XL + j * T::K(i) * kPad + c.t;
+    return fsm + T::XS + i * T::XL + j * T::K(i) * T::XP + c.t;
   }
   __device__ __forceinline__ const double* as(int i) const { return c.as + T::jlo(i) * kPad; }
 
   // S = Sp + X^red_w[run j] A_w for the K = 2 level (b = 2): cached A values, DFMA
   __device__ __forceinline__ void step_k2(const double (&Sp)[NV], int i, int j, double (&S)[NV]) const {
-    const double x0 = xs(i, j)[0], x1 = xs(i, j)[kPad];
+    const double x0 = xs(i, j)[0], x1 = xs(i, j)[T::XP];
 #pragma unroll
     for (int e = 0; e < NV; ++e) S[e] = fma(x1, a1[1][e], fma(x0, a1[0][e], Sp[e]));
   }
   template <int I>
   __device__ __forceinline__ void step(const double (&Sp)[NV], int j, double (&S)[NV]) const {
     if constexpr (B == 2 && T::K(I) == 2) step_k2(Sp, I, j, S);
-    else tree_step<T::K(I), NFR>(xs(I, j), as(I), c, Sp, S);
+    else tree_step<T::K(I), NFR, T::XP>(xs(I, j), as(I), c, Sp, S);
   }
 
   // leaves of parent run jp (level NF-1), generic shapes: Y store, g sums, smem rowacc[ch][leaf][t]
   __device__ __forceinline__ void leaves(const double (&Sp)[NV], int jp) {
     constexpr int I = NF - 1, KL = T::K(I), RP = T::runs(I) / B;
-    double* acc = fsm + T::ACC + c.ch * (T::LEAVES * kBundle) + c.t;
+    double* acc = fsm + T::ACC + c.ch * (T::LEAVES * BUN) + c.t;
     double v[B], pre[B];
     if constexpr (G > 0) {
 #pragma unroll
-      for (int q = 0; q < B; ++q) pre[q] = acc[(jp + q * RP) * kBundle];
+      for (int q = 0; q < B; ++q) pre[q] = acc[(jp + q * RP) * BUN];
     }
 #pragma unroll
     for (int q = 0; q < B; ++q) {
@@ -215,12 +220,12 @@ struct TreeRun {
 #pragma unroll
         for (int e = 0; e < NV; ++e) Y[e] = fma(x0, a0[0][e], Sp[e]);
         if constexpr (KL == 2) {
-          const double x1 = x[kPad];
+          const double x1 = x[T::XP];
 #pragma unroll
           for (int e = 0; e < NV; ++e) Y[e] = fma(x1, a0[KL - 1][e], Y[e]);
         }
       } else {
-        tree_step<KL, NFR>(xs(I, j), as(I), c, Sp, Y);
+        tree_step<KL, NFR, T::XP>(xs(I, j), as(I), c, Sp, Y);
       }
       tree_store<STY, NFR>(a, Y, j, c);
       if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0);
@@ -232,7 +237,7 @@ struct TreeRun {
       for (int q = 0; q < B; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], 2);
       if (c.tg == 0) {
 #pragma unroll
-        for (int q = 0; q < B; ++q) acc[(jp + q * RP) * kBundle] = pre[q] + v[q];
+        for (int q = 0; q < B; ++q) acc[(jp + q * RP) * BUN] = pre[q] + v[q];
       }
     }
   }
@@ -266,7 +271,7 @@ struct TreeRun {
     for (int n = 0; n < NN; ++n) {
       const int j2 = jl[4 * n];
       double S2[NV];
-      tree_step<4, NFR>(xs(I2, j2), as(I2), c, Sp, S2);
+      tree_step<4, NFR, T::XP>(xs(I2, j2), as(I2), c, Sp, S2);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double S1[NV];
@@ -354,22 +359,22 @@ struct TreeRun {
   }
 };
 
-template <int NF, int B, int G, bool STY, int NFR>
-__global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(const FineArgs a) {
-  using T = Tree<NF, B, NFR>;
-  using Run = TreeRun<NF, B, G, STY, NFR>;
+template <int NF, int B, int G, bool STY, int NFR, int BUN>
+__global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fine_tree(const FineArgs a) {
+  using T = Tree<NF, B, NFR, BUN>;
+  using Run = TreeRun<NF, B, G, STY, NFR, BUN>;
   constexpr int NT = T::THREADS, NW = T::WARPS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TreeCtx c;
-  c.wm = warp & 3;
-  c.ch = (warp >> 2) % T::CH;
-  c.grp = warp / (4 * T::CH);
+  c.wm = warp % T::RWN;
+  c.ch = (warp / T::RWN) % T::CH;
+  c.grp = warp / (T::RWN * T::CH);
   c.g = lane >> 2;
   c.tg = lane & 3;
   c.t = c.wm * 8 + c.g;
   c.cw = c.ch * 8 * NFR;
-  c.r0 = (int64_t)blockIdx.x * kBundle;
-  c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
+  c.r0 = (int64_t)blockIdx.x * BUN;
+  c.beff = (int)((a.Mroot - c.r0) < BUN ? (a.Mroot - c.r0) : BUN);
   const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
   const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
 
@@ -377,13 +382,13 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
   // doubles in HBM, read coalesced by 8-byte cp.async and transposed on the way into smem
 #pragma unroll
   for (int i = 0; i < NF; ++i) {
-    const int K = T::K(i), n = T::runs(i) * kBundle * K;
+    const int K = T::K(i), n = T::runs(i) * BUN * K;
     const double* src = a.lv[i].X + rep * a.xrep + c.r0 * (int64_t)K;
     double* dst = fsm + T::XS + i * T::XL;
     for (int e = tid; e < n; e += NT) {
-      const int j = e / (kBundle * K), r = e - j * (kBundle * K), t = r / K, q = r - t * K;
+      const int j = e / (BUN * K), r = e - j * (BUN * K), t = r / K, q = r - t * K;
       const bool ok = t < c.beff;
-      cp_async8(dst + (j * K + q) * kPad + t, ok ? src + (int64_t)j * a.Mroot * K + r : a.A, ok);
+      cp_async8(dst + (j * K + q) * T::XP + t, ok ? src + (int64_t)j * a.Mroot * K + r : a.A, ok);
     }
   }
   cp_async_commit();
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
   const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
   auto load_tile = [&](int buf, int c0) {
     double* as = fsm + buf * T::ABUF;
-    double* rs = fsm + T::ROOT + buf * (kBundle * kPad);
+    double* rs = fsm + T::ROOT + buf * (BUN * kPad);
     if (a.a_vec) {
       for (int e = tid; e < T::J * (kFineBN / 2); e += NT) {
         const int q = e >> 4, cc = (e & 15) * 2;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
         cp_async8(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     }
-    for (int e = tid; e < kBundle * (kFineBN / 2); e += NT) {
+    for (int e = tid; e < BUN * (kFineBN / 2); e += NT) {
       const int t = e >> 4, cc = (e & 15) * 2;
       const bool row_ok = root != nullptr && t < c.beff;
       const double* src = root + (c.r0 + t) * a.ldroot + c0 + cc;
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
     c.as = fsm + (ct & 1) * T::ABUF;
     if (ct + 1 < ntiles) load_tile((ct + 1) & 1, (ct + 1) * kFineBN);  // buffer freed by the last barrier
     double Sroot[T::NV];
-    run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (kBundle * kPad) + c.t * kPad);
+    run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (BUN * kPad) + c.t * kPad);
     run.tile(Sroot);
     cp_async_wait<0>();
     __syncthreads();  // tile ct + 1 landed and visible; buffers (ct & 1) free for tile ct + 2
@@ -447,10 +452,11 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
       // column-slice partial row sums -> complete row sums: slices ch > 0 park theirs in smem (the
       // X region is free after the last tile's barrier), slice 0 adds them in fixed order
       constexpr int NA = Run::NACC;
-      double* park = fsm + T::XS + ((c.grp * 4 + c.wm) * 32 + lane) * NA;
+      double* park = fsm + T::XS + ((c.grp * T::RWN + c.wm) * 32 + lane) * NA;
+      constexpr int PS = 2 * T::RWN * 32 * NA;   // one column slice's parked sums
       if (c.ch > 0) {
 #pragma unroll
-        for (int i = 0; i < NA; ++i) park[(c.ch - 1) * (8 * 32 * NA) + i] = run.racc[i];
+        for (int i = 0; i < NA; ++i) park[(c.ch - 1) * PS + i] = run.racc[i];
       }
       if constexpr (T::CH > 1) __syncthreads();
       if (c.ch == 0 && c.t < c.beff) {
@@ -458,17 +464,17 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
         for (int i = 0; i < NA; ++i) {
           double rs = run.racc[i];
 #pragma unroll
-          for (int h = 1; h < T::CH; ++h) rs += park[(h - 1) * (8 * 32 * NA) + i];
+          for (int h = 1; h < T::CH; ++h) rs += park[(h - 1) * PS + i];
           part += f_of_mean(a, (rs - pad) / a.tau);
         }
       }
     } else {
-      for (int e = tid; e < T::LEAVES * kBundle; e += NT) {
-        const int t = e % kBundle;
+      for (int e = tid; e < T::LEAVES * BUN; e += NT) {
+        const int t = e % BUN;
         if (t >= c.beff) continue;
         double rs = fsm[T::ACC + e];
 #pragma unroll
-        for (int h = 1; h < T::CH; ++h) rs += fsm[T::ACC + h * (T::LEAVES * kBundle) + e];
+        for (int h = 1; h < T::CH; ++h) rs += fsm[T::ACC + h * (T::LEAVES * BUN) + e];
         part += f_of_mean(a, (rs - pad) / a.tau);
       }
     }
@@ -486,22 +492,25 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR>::THREADS, 1) k_fine_tree(cons
 }
 
 template <int NF, int B, int G, bool STY>
-static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
-  constexpr int NFR = RQMC_TREE_NFR;
-  using T = Tree<NF, B, NFR>;
+static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
+  constexpr int NFR = RQMC_TREE_NFR, BUN = RQMC_TREE_BUNDLE;
+  using T = Tree<NF, B, NFR, BUN>;
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
   }
-  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR>, T::SMEM);
+  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN>, T::SMEM);
   if (e != cudaSuccess) return e;
-  k_fine_tree<NF, B, G, STY, NFR><<<dim3((unsigned)nb, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
+  const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
+  if (nbt > 2 * nb) return cudaErrorInvalidValue;   // workspace holds 2 nb partials per replica
+  *nparts = nbt;
+  k_fine_tree<NF, B, G, STY, NFR, BUN><<<dim3((unsigned)nbt, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
 template <int NF, int B>
 static bool tree_matches(const FineArgs& a) {
-  using T = Tree<NF, B, RQMC_TREE_NFR>;
+  using T = Tree<NF, B, RQMC_TREE_NFR, RQMC_TREE_BUNDLE>;
   if (a.NF != NF) return false;
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
@@ -511,27 +520,27 @@ static bool tree_matches(const FineArgs& a) {
 }
 
 template <int NF, int B>
-static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
+static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* np) {
   const bool sty = a.Y != nullptr;
   switch (a.fk) {
-    case -1: return launch_tree_t<NF, B, 0, true>(a, nb, nrep, st);
-    case 1: return sty ? launch_tree_t<NF, B, 2, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 2, false>(a, nb, nrep, st);
-    case 2: return sty ? launch_tree_t<NF, B, 3, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 3, false>(a, nb, nrep, st);
-    default: return sty ? launch_tree_t<NF, B, 1, true>(a, nb, nrep, st) : launch_tree_t<NF, B, 1, false>(a, nb, nrep, st);
+    case -1: return launch_tree_t<NF, B, 0, true>(a, nb, nrep, st, np);
+    case 1: return sty ? launch_tree_t<NF, B, 2, true>(a, nb, nrep, st, np) : launch_tree_t<NF, B, 2, false>(a, nb, nrep, st, np);
+    case 2: return sty ? launch_tree_t<NF, B, 3, true>(a, nb, nrep, st, np) : launch_tree_t<NF, B, 3, false>(a, nb, nrep, st, np);
+    default: return sty ? launch_tree_t<NF, B, 1, true>(a, nb, nrep, st, np) : launch_tree_t<NF, B, 1, false>(a, nb, nrep, st, np);
   }
 }
 
 // returns cudaErrorNotSupported when no compile-time tree matches
-cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
+cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* np) {
   if (a.Y == nullptr && a.fk < 0) return cudaErrorNotSupported;
-  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, nrep, st);
-  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, nrep, st);
-  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, nrep, st);
-  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, nrep, st);
-  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, nrep, st);
-  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, nrep, st);
-  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, nrep, st);
-  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, nrep, st);
+  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, nrep, st, np);
+  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, nrep, st, np);
+  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, nrep, st, np);
+  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, nrep, st, np);
+  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, nrep, st, np);
+  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, nrep, st, np);
+  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, nrep, st, np);
+  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, nrep, st, np);
   return cudaErrorNotSupported;
 }
 
