@@ -189,7 +189,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
     nu = (a.M + a.Mp - 1) / a.Mp;
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
-  const int sm = BM == 128 ? gemm_smem_bytes<128>() : gemm_smem_bytes<64>();
+  const int sm = BM == 128 ? gemm_smem_bytes<128>() : (BM == 64 ? gemm_smem_bytes<64>() : gemm_smem_bytes<32>());
 #ifndef RQMC_GEMM_WMF
 #define RQMC_GEMM_WMF 4
 #endif
@@ -207,6 +207,8 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
   };
   if (BM == 128)
     return vec ? go(k_level_gemm<128, 2, WMF>, 128 / (8 * WMF) * 64) : go(k_level_gemm<128, 1, WMF>, 128 / (8 * WMF) * 64);
+  if (BM == 32)
+    return vec ? go(k_level_gemm<32, 2, WMF>, 32 / (8 * WMF) * 64) : go(k_level_gemm<32, 1, WMF>, 32 / (8 * WMF) * 64);
   return vec ? go(k_level_gemm<64, 2, WMF>, 64 / (8 * WMF) * 64) : go(k_level_gemm<64, 1, WMF>, 64 / (8 * WMF) * 64);
 }
 
