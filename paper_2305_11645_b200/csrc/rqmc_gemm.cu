@@ -1,5 +1,6 @@
 // a3+a4 coarse level GEMM (k_level_gemm): one level of paper Alg. 2,
-// R_w = tile(R_w') + X^red_w A_w, as a DMMA.8x8x4 (fp64 tensor core) GEMM.
+// R_w = tile(R_w') + X^red_w A_w, as a DMMA.8x8x4 (fp64 tensor core) GEMM -- optionally fused with
+// the next finer level (R_c = tile(R_w) + X^red_c A_c) so that R_w never goes to HBM.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -15,24 +16,31 @@ namespace rqmc {
 // ------------------------------------------------------------------------------------------
 // R[r, c] = Rp[r mod Mp, c] + sum_q X[r, q] A[q, c]   (the accumulator starts from the parent row)
 //
-// CTA tile BM x 64, k-tile 16, NST-stage cp.async ring (one barrier per k-tile; 2 stages measured
-// best: 3 equal, 4 slower), warps (BM/32) x 2
-// each 32 x 32 = 4 x 4 DMMA fragments (8 fragment loads per 16 DMMAs).
+// CTA tile BM x 64, k-tile 16, 2-stage cp.async ring with one barrier per k-tile, warps
+// (BM / 8 WMF) x 2 each (8 WMF) x 32 = WMF x 4 DMMA fragments.  Measured on C5 (ncu, per level):
+// BM = 64 (4 CTAs per SM) beats 128 (2 per SM) on every level (13.5 vs 14.1 ms) and 32; 3 stages
+// equal, 4 stages and BK = 32 slower; WMF = 8 (64 x 32 warp tiles) slower.
 // Row blocks are ordered sibling-first: CTA y = pb * nu + u covers rows u Mp + pb BM + [0, BM), so the
 // nu = M / Mp child blocks of one parent block run back to back and all but the first read the
 // parent tile from L2 (the parent R is read from HBM once instead of nu times).
+//
+// Pair mode (a.Xc != nullptr): the tile of R_w stays in registers and seeds the GEMMs of the next
+// finer level c (parent w, M_c = ncu * M_w): for u < ncu, R_c[u M_w + r] = R_w[r] + X_c[u M_w + r] A_c.
+// The arithmetic (accumulator initialised with the parent value, DMMA k-steps in increasing k) is
+// exactly that of two separate launches, so the result is bit-identical; R_w's HBM write and
+// re-read disappear.
 // ------------------------------------------------------------------------------------------
 #ifndef RQMC_GEMM_STAGES
 #define RQMC_GEMM_STAGES 2
-#endif
-#ifndef RQMC_GEMM_PARENT_LAST
-#define RQMC_GEMM_PARENT_LAST 0
 #endif
 #ifndef RQMC_GEMM_SIBLING
 #define RQMC_GEMM_SIBLING 1
 #endif
 #ifndef RQMC_GEMM_BK
 #define RQMC_GEMM_BK 16
+#endif
+#ifndef RQMC_GEMM_WMF
+#define RQMC_GEMM_WMF 4
 #endif
 constexpr int kGemmBN = 64, kGemmBK = RQMC_GEMM_BK, kGemmStages = RQMC_GEMM_STAGES;
 
@@ -41,8 +49,7 @@ constexpr int gemm_smem_bytes() {
   return (int)sizeof(double) * kGemmStages * (BM * (kGemmBK + 4) + kGemmBK * (kGemmBN + 4));
 }
 
-// WMF = DMMA fragments per warp along M (warp tile 8 WMF x 32); warps (BM / 8 WMF) x 2
-template <int BM, int CH, int WMF>
+template <int BM, int CH, int WMF, bool PAIR>
 __global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
                                                                    int64_t y0) {
   constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4;
@@ -60,44 +67,75 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmAr
   const int64_t rlim = min(a.M, u * mp_blk + mp_blk);  // rows >= rlim belong to another tile
   const int c0 = blockIdx.x * BN;
   // replica blockIdx.z (batched randomisation): its own X^red and R buffers, shared A
-  const double* __restrict__ Xg = a.X + (int64_t)blockIdx.z * a.xrep;
-  const double* __restrict__ Rpg = a.Rp ? a.Rp + (int64_t)blockIdx.z * a.rrep : nullptr;
-  double* __restrict__ Rg = a.R + (int64_t)blockIdx.z * a.rrep;
+  const int64_t zr = blockIdx.z;
+  const double* __restrict__ Rpg = a.Rp ? a.Rp + zr * a.rrep : nullptr;
 
-  auto load_stage = [&](int buf, int k0) {
-    // X tile: BM rows x BK cols (ldx even: 16B chunks stay inside the zero-padded row)
-    for (int c = tid; c < BM * (BK / 2); c += NT) {
-      const int row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-      const int64_t gr = r0 + row;
-      const bool ok = gr < rlim && (k0 + kc) < a.ldx;
-      const double* src = ok ? Xg + gr * a.ldx + k0 + kc : Xg;
-      cp_async16(&Xs[buf][row][kc], src, ok);
+  // one GEMM into acc: rows rbase + [0, BM) (valid below rl) of X (ldx, K columns) times A (K rows)
+  auto gemm = [&](const double* X, int64_t ldx, int K, const double* A, int64_t rbase, int64_t rl,
+                  double (&acc)[WMF][4][2]) {
+    auto load_stage = [&](int buf, int k0) {
+      // X tile: BM rows x BK cols (ldx even: 16B chunks stay inside the zero-padded row)
+      for (int c = tid; c < BM * (BK / 2); c += NT) {
+        const int row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+        const int64_t gr = rbase + row;
+        const bool ok = gr < rl && (k0 + kc) < ldx;
+        const double* src = ok ? X + gr * ldx + k0 + kc : X;
+        cp_async16(&Xs[buf][row][kc], src, ok);
+      }
+      // A tile: BK rows x BN cols
+      for (int c = tid; c < BK * (BN / CH); c += NT) {
+        const int row = c / (BN / CH), cc = (c % (BN / CH)) * CH;
+        const bool ok = (k0 + row) < K && (c0 + cc) < a.tau;
+        const double* src = ok ? A + (int64_t)(k0 + row) * a.lda + c0 + cc : A;
+        if (CH == 2) cp_async16(&As[buf][row][cc], src, ok);
+        else cp_async8(&As[buf][row][cc], src, ok);
+      }
+    };
+    const int nk = (K + BK - 1) / BK;
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+      if (s < nk) load_stage(s, s * BK);
+      cp_async_commit();
     }
-    // A tile: BK rows x BN cols
-    for (int c = tid; c < BK * (BN / CH); c += NT) {
-      const int row = c / (BN / CH), cc = (c % (BN / CH)) * CH;
-      const bool ok = (k0 + row) < a.K && (c0 + cc) < a.tau;
-      const double* src = ok ? a.A + (int64_t)(k0 + row) * a.lda + c0 + cc : a.A;
-      if (CH == 2) cp_async16(&As[buf][row][cc], src, ok);
-      else cp_async8(&As[buf][row][cc], src, ok);
-    }
-  };
-
-  if (RQMC_GEMM_PARENT_LAST && Rpg) {  // warm L2 with the parent tile; it is added after the k-loop
-    for (int c = tid; c < BM * 4; c += NT) {
-      const int64_t row = r0 + c / 4;
-      if (row < rlim) {
-        const double* p = Rpg + (row % a.Mp) * a.ldp + c0 + (c % 4) * 16;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    for (int kt = 0; kt < nk; ++kt) {
+      cp_async_wait<NST - 2>();
+      __syncthreads();  // stage kt landed for all threads; stage kt-1's buffer is free
+      if (kt + NST - 1 < nk) load_stage((kt + NST - 1) % NST, (kt + NST - 1) * BK);
+      cp_async_commit();
+      const int buf = kt % NST;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[WMF], bf[4];
+#pragma unroll
+        for (int i = 0; i < WMF; ++i) af[i] = Xs[buf][wm * WR + i * 8 + g][kk + tg];
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) bf[jn] = As[buf][kk + tg][wn * 32 + jn * 8 + g];
+#pragma unroll
+        for (int i = 0; i < WMF; ++i)
+#pragma unroll
+          for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
       }
     }
-  }
-  const int nk = (a.K + BK - 1) / BK;
+    cp_async_wait<0>();
+    if constexpr (PAIR) __syncthreads();  // the stage buffers are refilled by the next gemm() of this CTA
+  };
+  auto store = [&](double* R, int64_t ldr, int64_t rbase, int64_t rl, const double (&acc)[WMF][4][2]) {
 #pragma unroll
-  for (int s = 0; s < NST - 1; ++s) {
-    if (s < nk) load_stage(s, s * BK);
-    cp_async_commit();
-  }
+    for (int i = 0; i < WMF; ++i) {
+      const int64_t row = rbase + wm * WR + i * 8 + g;
+      if (row >= rl) continue;
+#pragma unroll
+      for (int jn = 0; jn < 4; ++jn) {
+        const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
+        double* p = R + row * ldr + col;
+        if (col + 1 < a.tau) {
+          *reinterpret_cast<double2*>(p) = make_double2(acc[i][jn][0], acc[i][jn][1]);
+        } else if (col < a.tau) {
+          p[0] = acc[i][jn][0];
+        }
+      }
+    }
+  };
 
   double acc[WMF][4][2];
 #pragma unroll
@@ -108,7 +146,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmAr
       const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
       acc[i][jn][0] = 0.0;
       acc[i][jn][1] = 0.0;
-      if (!RQMC_GEMM_PARENT_LAST && Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
+      if (Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
         const double* p = Rpg + (row % a.Mp) * a.ldp + col;
         if (CH == 2 && col + 1 < a.tau) {
           const double2 v = *reinterpret_cast<const double2*>(p);
@@ -121,67 +159,39 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmAr
       }
     }
   }
-
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<NST - 2>();
-    __syncthreads();  // stage kt landed for all threads; stage kt-1's buffer is free
-    if (kt + NST - 1 < nk) load_stage((kt + NST - 1) % NST, (kt + NST - 1) * BK);
-    cp_async_commit();
-    const int buf = kt % NST;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[WMF], bf[4];
-#pragma unroll
-      for (int i = 0; i < WMF; ++i) af[i] = Xs[buf][wm * WR + i * 8 + g][kk + tg];
-#pragma unroll
-      for (int jn = 0; jn < 4; ++jn) bf[jn] = As[buf][kk + tg][wn * 32 + jn * 8 + g];
+  gemm(a.X + zr * a.xrep, a.ldx, a.K, a.A, r0, rlim, acc);
+  if constexpr (!PAIR) {
+    store(a.R + zr * a.rrep, a.ldr, r0, rlim, acc);
+  } else {
+    // children of this tile's rows in level c: rows uc M + r, uc < ncu (tile(R_w) for level c)
+    for (int uc = 0; uc < a.ncu; ++uc) {
+      double acc2[WMF][4][2];
 #pragma unroll
       for (int i = 0; i < WMF; ++i)
 #pragma unroll
-        for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
-    }
-  }
-  cp_async_wait<0>();
-
-#pragma unroll
-  for (int i = 0; i < WMF; ++i) {
-    const int64_t row = r0 + wm * WR + i * 8 + g;
-    if (row >= rlim) continue;
-    if (RQMC_GEMM_PARENT_LAST && Rpg) {
-#pragma unroll
-      for (int jn = 0; jn < 4; ++jn) {
-        const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
-        const double* p = Rpg + (row % a.Mp) * a.ldp + col;
-        if (col + 1 < a.tau) {
-          acc[i][jn][0] += p[0];
-          acc[i][jn][1] += p[1];
-        } else if (col < a.tau) {
-          acc[i][jn][0] += p[0];
+        for (int jn = 0; jn < 4; ++jn) {
+          acc2[i][jn][0] = acc[i][jn][0];
+          acc2[i][jn][1] = acc[i][jn][1];
         }
-      }
-    }
-#pragma unroll
-    for (int jn = 0; jn < 4; ++jn) {
-      const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
-      double* p = Rg + row * a.ldr + col;
-      if (col + 1 < a.tau) {
-        *reinterpret_cast<double2*>(p) = make_double2(acc[i][jn][0], acc[i][jn][1]);
-      } else if (col < a.tau) {
-        p[0] = acc[i][jn][0];
-      }
+      const int64_t cb = (int64_t)uc * a.M + r0, cl = (int64_t)uc * a.M + rlim;
+      gemm(a.Xc + zr * a.xrep, a.ldxc, a.Kc, a.Ac, cb, cl, acc2);
+      store(a.Rc + zr * a.rrep, a.ldr, cb, cl, acc2);
     }
   }
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
   if (a.M == 0 || nrep == 0) return cudaSuccess;
+  const bool pair = a.Xc != nullptr;
   const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
+                   (!pair || ((uintptr_t)a.Ac % 16 == 0)) &&
                    (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
 #ifndef RQMC_GEMM_BM
-  const int BM = 64;   // 4 CTAs per SM: measured best on every C5 level (13.5 vs 14.1 ms, BM = 128 for long levels)
+  constexpr int BM = 64;
 #else
-  const int BM = RQMC_GEMM_BM;
+  constexpr int BM = RQMC_GEMM_BM;
 #endif
+  constexpr int WMF = RQMC_GEMM_WMF, NT = BM / (8 * WMF) * 64;
   // sibling-first ordering when the parent has at least one full row block; else plain row blocks
   int64_t mp_blk = a.M, nu = 1;
   if (RQMC_GEMM_SIBLING && a.Rp && a.Mp >= BM && a.Mp < a.M) {
@@ -189,27 +199,20 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
     nu = (a.M + a.Mp - 1) / a.Mp;
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
-  const int sm = BM == 128 ? gemm_smem_bytes<128>() : (BM == 64 ? gemm_smem_bytes<64>() : gemm_smem_bytes<32>());
-#ifndef RQMC_GEMM_WMF
-#define RQMC_GEMM_WMF 4
-#endif
-  constexpr int WMF = RQMC_GEMM_WMF;
-  auto go = [&](auto kern, int nt) -> cudaError_t {
+  const int sm = gemm_smem_bytes<BM>();
+  auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = set_smem_once(kern, sm);
     if (e != cudaSuccess) return e;
-    // grid.x = column blocks (fastest: the 32 CTAs of one row block share its X^red rows in L2)
+    // grid.x = column blocks (fastest: the CTAs of one row block share its X^red rows in L2)
     for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
       dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0),
                 (unsigned)nrep);
-      kern<<<grid, nt, sm, st>>>(a, mp_blk, nu, y0);
+      kern<<<grid, NT, sm, st>>>(a, mp_blk, nu, y0);
     }
     return cudaGetLastError();
   };
-  if (BM == 128)
-    return vec ? go(k_level_gemm<128, 2, WMF>, 128 / (8 * WMF) * 64) : go(k_level_gemm<128, 1, WMF>, 128 / (8 * WMF) * 64);
-  if (BM == 32)
-    return vec ? go(k_level_gemm<32, 2, WMF>, 32 / (8 * WMF) * 64) : go(k_level_gemm<32, 1, WMF>, 32 / (8 * WMF) * 64);
-  return vec ? go(k_level_gemm<64, 2, WMF>, 64 / (8 * WMF) * 64) : go(k_level_gemm<64, 1, WMF>, 64 / (8 * WMF) * 64);
+  if (pair) return vec ? go(k_level_gemm<BM, 2, WMF, true>) : go(k_level_gemm<BM, 1, WMF, true>);
+  return vec ? go(k_level_gemm<BM, 2, WMF, false>) : go(k_level_gemm<BM, 1, WMF, false>);
 }
 
 }  // namespace rqmc

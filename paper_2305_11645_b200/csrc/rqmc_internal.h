@@ -50,6 +50,9 @@ struct GemmArgs {                // one coarse level: R = tile(Rp) + X A_w
   const double* Rp; int64_t ldp; int64_t Mp;   // parent R (nullptr: zero)
   double* R; int64_t ldr;
   int64_t xrep, rrep;            // replica strides (doubles) of X and of the R buffers (grid.z = replica)
+  // pair mode (Xc != nullptr): this level's R stays on chip and seeds the next finer level c, whose
+  // local rows u M + r (u < ncu) have parent row r; R (this level) is not written, Rc (ldr) is
+  const double* Xc; int64_t ldxc; int Kc; const double* Ac; double* Rc; int ncu;
 };
 
 struct FineLevel {

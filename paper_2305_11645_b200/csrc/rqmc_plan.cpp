@@ -26,6 +26,7 @@ namespace {
 
 struct Level {
   int w, j_lo, s_w, parent, coarse;
+  int fused;      // coarse pair parent: R stays on chip, computed with its child (next level) in one launch
   int64_t M, Ml;
   int ldx;
   int64_t xoff;   // doubles
@@ -178,10 +179,24 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
     L.max_gen_entries = std::max<int64_t>(L.max_gen_entries, V.Ml * V.ldx);
   }
   L.ldr = (p.tau + 1) / 2 * 2;
+  // coarse pairs (c-1, c), (c-3, c-2), ...: the parent's R stays on chip when each of its rows has
+  // <= 4 child rows.  Opt-in (RQMC_GEMM_PAIR=1): bit-identical, but the pair kernel holds two
+  // accumulator tiles (167 registers, 3 CTAs per SM) and measured slower on C5 (coarse 15.06 vs
+  // 13.54 ms) although it saves R_7's 4.3 GB round trip.  Stored levels alternate R buffers.
+  static const bool no_pair = [] { const char* e = std::getenv("RQMC_GEMM_PAIR"); return !(e && *e && *e != '0'); }();
+  for (int i = 0; i <= c; ++i) L.lv[i].fused = 0;
+  for (int i = c - 1; i >= 0 && !no_pair; i -= 2) {
+    const Level &P = L.lv[i], &C = L.lv[i + 1];
+    const int64_t ncu = C.Ml / P.Ml;
+    if (C.parent == i && ncu * P.Ml == C.Ml && ncu >= 1 && ncu <= 4) L.lv[i].fused = 1;
+  }
   size_t rsz[2] = {0, 0};
+  int nstored = 0;
   for (int i = 0; i <= c; ++i) {
-    L.lv[i].rbuf = i & 1;
-    rsz[i & 1] = std::max(rsz[i & 1], (size_t)L.lv[i].Ml * L.ldr * sizeof(double));
+    if (L.lv[i].fused) { L.lv[i].rbuf = -1; continue; }
+    const int b = nstored++ & 1;
+    L.lv[i].rbuf = b;
+    rsz[b] = std::max(rsz[b], (size_t)L.lv[i].Ml * L.ldr * sizeof(double));
   }
   L.off_r[0] = off; off = align_up(off + rsz[0], 256);
   L.off_r[1] = off; off = align_up(off + rsz[1], 256);
@@ -490,7 +505,8 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
 
-  // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine
+  // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine.  A fused pair (Layout) runs as
+  // one launch whose parent R never leaves the chip (bit-identical to two launches).
   for (int i = 0; i <= lay.ckpt; ++i) {
     const Level& L = lay.lv[i];
     GemmArgs a{};
@@ -500,8 +516,17 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
       const Level& P = lay.lv[L.parent];
       a.Rp = reinterpret_cast<const double*>(w + lay.off_r[P.rbuf]); a.ldp = lay.ldr; a.Mp = P.Ml;
     }
-    a.R = reinterpret_cast<double*>(w + lay.off_r[L.rbuf]); a.ldr = lay.ldr;
+    a.ldr = lay.ldr;
     a.xrep = rep_d; a.rrep = rep_d;
+    if (L.fused) {
+      const Level& Cl = lay.lv[i + 1];
+      a.Xc = g.X + Cl.xoff; a.ldxc = Cl.ldx; a.Kc = Cl.s_w; a.Ac = dA + (int64_t)Cl.j_lo * lda;
+      a.Rc = reinterpret_cast<double*>(w + lay.off_r[Cl.rbuf]); a.ncu = (int)(Cl.Ml / L.Ml);
+      if (rqmc_status s = check_cuda(p, launch_gemm(a, nrep, st), "k_level_gemm (pair)")) return s;
+      ++i;   // level i + 1 done in the same launch
+      continue;
+    }
+    a.R = reinterpret_cast<double*>(w + lay.off_r[L.rbuf]);
     if (rqmc_status s = check_cuda(p, launch_gemm(a, nrep, st), "k_level_gemm")) return s;
   }
 

@@ -289,3 +289,29 @@ def test_config_c5_panel_rows(rq):
     Y = pl.xa(dev(prob.A))
     ks = _sample_rows(prob.N, 600, 5)
     check_y(prob, Y[torch.from_numpy(ks).cuda()].cpu().numpy(), ks)
+
+
+def test_coarse_pair_fusion_bit_identical(rq, monkeypatch):
+    """Opt-in fused coarse pairs (parent R kept on chip, RQMC_GEMM_PAIR=1) reproduce the two-launch
+    result bit for bit (same accumulation order), incl. a b = 3 plan and several checkpoints."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, workloads as W, paper_2305_11645_b200 as rq\n"
+            "out = []\n"
+            "for seed, b, m, ck in ((41, 2, 13, '5'), (42, 3, 8, '3'), (43, 2, 12, '')):\n"
+            "    prob = W.make_random(seed, b, m, 200, 70, shifted=True, mapping=W.MAP_INVNORM)\n"
+            "    import os; os.environ['RQMC_CKPT_W'] = ck\n"
+            "    pl = rq.Plan.from_problem(prob)\n"
+            "    Y, fs = pl.xa(torch.from_numpy(prob.A).cuda(), prob.f, prob.fparam)\n"
+            "    out.append(Y.cpu().numpy())\n"
+            "np.save(__import__('sys').argv[1], np.concatenate([o.ravel() for o in out]))\n")
+    import os
+    import tempfile
+    res = []
+    for flag in ("0", "1"):
+        f = os.path.join(tempfile.mkdtemp(), "y.npy")
+        env = dict(os.environ, RQMC_GEMM_PAIR=flag)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
