@@ -399,9 +399,32 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   // (One 256-byte cp.async.bulk per row completing on an mbarrier measured 2.1 ms slower on C5: the
   // 95 small bulk requests per tile serialise in the copy engine.)
   const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
+  // fast path (every full tile of a 16-byte-aligned A and root, full bundle): each thread's chunks are
+  // fixed rows / columns, so addresses are base + compile-time multiples of a runtime stride
+  constexpr int CPR = kFineBN / 2;                          // 16-byte chunks per row
+  constexpr int RPP = NT / CPR;                             // rows per pass of all threads
+  constexpr int UA = (T::J + RPP - 1) / RPP, UR = (BUN + RPP - 1) / RPP;
+  const bool fast = a.a_vec && root != nullptr && c.beff == BUN && (a.ldroot % 2) == 0 &&
+                    ((uintptr_t)root % 16) == 0;
+  const int fq = tid / CPR, fcc = (tid % CPR) * 2;
+  const double* fa = a.A + (int64_t)fq * a.lda + fcc;
+  const double* fr = root ? root + (c.r0 + fq) * a.ldroot + fcc : nullptr;
+  const int fo = fq * kPad + fcc;
   auto load_tile = [&](int buf, int c0) {
     double* as = fsm + buf * T::ABUF;
     double* rs = fsm + T::ROOT + buf * (BUN * kPad);
+    if (fast && c0 + kFineBN <= a.tau) {
+#pragma unroll
+      for (int u = 0; u < UA; ++u)
+        if (u + 1 < UA || fq + u * RPP < T::J)
+          cp_async16(as + fo + u * RPP * kPad, fa + (int64_t)u * RPP * a.lda + c0, true);
+#pragma unroll
+      for (int u = 0; u < UR; ++u)
+        if (u + 1 < UR || fq + u * RPP < BUN)
+          cp_async16(rs + fo + u * RPP * kPad, fr + (int64_t)u * RPP * a.ldroot + c0, true);
+      cp_async_commit();
+      return;
+    }
     if (a.a_vec) {
       for (int e = tid; e < T::J * (kFineBN / 2); e += NT) {
         const int q = e >> 4, cc = (e & 15) * 2;
