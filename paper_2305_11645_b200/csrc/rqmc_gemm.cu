@@ -73,22 +73,28 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmAr
   // one GEMM into acc: rows rbase + [0, BM) (valid below rl) of X (ldx, K columns) times A (K rows)
   auto gemm = [&](const double* X, int64_t ldx, int K, const double* A, int64_t rbase, int64_t rl,
                   double (&acc)[WMF][4][2]) {
+    // each thread's chunks are fixed (row, column) pairs: rows xr + u XRP of X, rows ar + u ARP of A
+    constexpr int XCPR = BK / 2, XRP = NT / XCPR, ACPR = BN / CH, ARP = NT / ACPR;
+    static_assert(NT % XCPR == 0 && NT % ACPR == 0, "loader shape");
+    const int xr = tid / XCPR, xk = (tid % XCPR) * 2, ar = tid / ACPR, ac = (tid % ACPR) * CH;
+    const double* Xt = X + (rbase + xr) * ldx + xk;
+    const double* At = A + (int64_t)ar * a.lda + c0 + ac;
+    const bool acol = c0 + ac < a.tau;
     auto load_stage = [&](int buf, int k0) {
       // X tile: BM rows x BK cols (ldx even: 16B chunks stay inside the zero-padded row)
-      for (int c = tid; c < BM * (BK / 2); c += NT) {
-        const int row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-        const int64_t gr = rbase + row;
-        const bool ok = gr < rl && (k0 + kc) < ldx;
-        const double* src = ok ? X + gr * ldx + k0 + kc : X;
-        cp_async16(&Xs[buf][row][kc], src, ok);
+      const bool kok = k0 + xk < ldx;
+#pragma unroll
+      for (int u = 0; u < BM / XRP; ++u) {
+        const bool ok = kok && rbase + xr + u * XRP < rl;
+        cp_async16(&Xs[buf][xr + u * XRP][xk], ok ? Xt + (int64_t)u * XRP * ldx + k0 : X, ok);
       }
       // A tile: BK rows x BN cols
-      for (int c = tid; c < BK * (BN / CH); c += NT) {
-        const int row = c / (BN / CH), cc = (c % (BN / CH)) * CH;
-        const bool ok = (k0 + row) < K && (c0 + cc) < a.tau;
-        const double* src = ok ? A + (int64_t)(k0 + row) * a.lda + c0 + cc : A;
-        if (CH == 2) cp_async16(&As[buf][row][cc], src, ok);
-        else cp_async8(&As[buf][row][cc], src, ok);
+#pragma unroll
+      for (int u = 0; u < BK / ARP; ++u) {
+        const bool ok = acol && k0 + ar + u * ARP < K;
+        const double* src = ok ? At + (int64_t)(k0 + u * ARP) * a.lda : A;
+        if (CH == 2) cp_async16(&As[buf][ar + u * ARP][ac], src, ok);
+        else cp_async8(&As[buf][ar + u * ARP][ac], src, ok);
       }
     };
     const int nk = (K + BK - 1) / BK;
