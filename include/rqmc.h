@@ -145,7 +145,10 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
                     double* d_fsum, void* dwork, size_t wbytes, void* stream);
 
 /* End-to-end form with HOST buffers: copies hA (pinned or pageable) into the workspace, runs
- * rqmc_qn and copies the local f-sum back into *h_fsum; synchronises the stream before returning. */
+ * rqmc_qn and copies the local f-sum back into *h_fsum; synchronises the stream before returning.
+ * The H2D copy of A runs on a plan-owned copy stream, overlapped with the point generation (which
+ * does not read A); the GEMMs wait for it (full overlap needs pinned hA).  Not reentrant per plan
+ * (serialised by a plan mutex). */
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream);
 

@@ -80,6 +80,10 @@ struct rqmc_plan_s {
   std::vector<std::unique_ptr<Layout>> lay_cache;
   // device tables (uploaded once, lazily)
   std::once_flag up_once;
+  // rqmc_qn_host: copy stream + events so that the H2D of A overlaps the point generation
+  std::mutex h2d_mu;
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t h2d_ev[2] = {nullptr, nullptr};
   cudaError_t up_err = cudaSuccess;
   uint64_t* d_z = nullptr;
   double* d_shift = nullptr;
@@ -380,6 +384,9 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
 void rqmc_plan_destroy(rqmc_plan_t p) {
   if (!p) return;
   for (auto e : p->prof_ev) cudaEventDestroy(e);
+  for (auto e : p->h2d_ev)
+    if (e) cudaEventDestroy(e);
+  if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->d_z) cudaFree(p->d_z);
   if (p->d_shift) cudaFree(p->d_shift);
   if (p->d_C) cudaFree(p->d_C);
@@ -489,6 +496,7 @@ struct RunRand {
 };
 
 rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_t rep_bytes, const RunRand& rr,
+                     cudaEvent_t a_ready /* nullable: A is produced on another stream; wait before the GEMMs */,
                      const double* dA,
                      int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
                      cudaStream_t st) {
@@ -504,6 +512,8 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
+  if (a_ready)
+    if (rqmc_status s = check_cuda(p, cudaStreamWaitEvent(st, a_ready, 0), "wait for A")) return s;
 
   // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine.  A fused pair (Layout) runs as
   // one launch whose parent R never leaves the chip (bit-identical to two launches).
@@ -585,8 +595,8 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   if (!want_f && !dY) return RQMC_OK;
   if (rqmc_status s = upload(p)) return s;
   const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
-  return run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, dA, lda, dY, ldy, f, fparam, d_fsum,
-                  st);
+  return run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, nullptr, dA, lda, dY, ldy, f, fparam,
+                  d_fsum, st);
 }
 
 // bytes of one replica's workspace slice [X^red][R0][R1][partials] and of a chunk of n replicas
@@ -616,14 +626,33 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
   if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
   if (wbytes < p->L1.total) return fail(p, RQMC_EINVAL, "workspace too small");
   if (lda < p->tau) return fail(p, RQMC_EDIM, "lda < tau");
+  if (f == RQMC_F_NONE) return fail(p, RQMC_EINVAL, "rqmc_qn_host needs f");
+  if (rqmc_status s = check_f(p, f, fparam)) return s;
+  if (rqmc_status s = upload(p)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(dwork);
   double* dA = reinterpret_cast<double*>(w + p->L1.off_a);
   double* dsum = reinterpret_cast<double*>(w + p->L1.off_fsum);
-  cudaError_t e = cudaMemcpy2DAsync(dA, (size_t)p->L1.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
-                                    (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, st);
+  // H2D of A on a copy stream, overlapped with the point generation (which does not read A); the
+  // GEMMs wait for it.  Ordered after earlier work on st (ev[0]) so A's staging buffer is free.
+  std::lock_guard<std::mutex> lk(p->h2d_mu);
+  cudaError_t e = cudaSuccess;
+  if (!p->h2d_stream) {
+    e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&p->h2d_ev[i], cudaEventDisableTiming);
+    if (rqmc_status s = check_cuda(p, e, "copy stream")) return s;
+  }
+  e = cudaEventRecord(p->h2d_ev[0], st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h2d_stream, p->h2d_ev[0], 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(dA, (size_t)p->L1.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
+                          (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, p->h2d_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(p->h2d_ev[1], p->h2d_stream);
   if (rqmc_status s = check_cuda(p, e, "H2D A")) return s;
-  if (rqmc_status s = rqmc_qn(p, dA, p->L1.ldr, f, fparam, dsum, dwork, wbytes, stream)) return s;
+  const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
+  if (rqmc_status s = run_core(p, p->L1, 1, w, p->L1.off_fsum, rr, p->h2d_ev[1], dA, p->L1.ldr, nullptr, 0, f, fparam,
+                               dsum, st))
+    return s;
   e = cudaMemcpyAsync(h_fsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   return check_cuda(p, e, "D2H fsum");
@@ -693,7 +722,8 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
     if (p->kind == RQMC_LATTICE) rr.shift = reinterpret_cast<const double*>(dtab);
     else if (p->kind == RQMC_DIGITAL_NET) rr.dshift = reinterpret_cast<const uint64_t*>(dtab);
     else rr.seeds = reinterpret_cast<const uint64_t*>(dtab);
-    if (rqmc_status s = run_core(p, *lay, n, w, rep_slice_bytes(*lay), rr, dA, lda, nullptr, 0, f, fparam, d_fsum + r0, st))
+    if (rqmc_status s = run_core(p, *lay, n, w, rep_slice_bytes(*lay), rr, nullptr, dA, lda, nullptr, 0, f, fparam,
+                                 d_fsum + r0, st))
       return s;
   }
   return RQMC_OK;
