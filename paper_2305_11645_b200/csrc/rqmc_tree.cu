@@ -35,6 +35,9 @@ namespace rqmc {
 // Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36
 // doubles (bank-conflict-free fragment loads); columns >= tau are zero in the A slab and root tile.
 // ------------------------------------------------------------------------------------------
+#ifndef RQMC_S2_FIRST           // bottom block: both K = 4 nodes' DMMAs before the DFMA work (17.02 vs
+#define RQMC_S2_FIRST 1         // 17.34 ms on C5); computing both children of the level above first: slower
+#endif
 #ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
 #define RQMC_TREE_BUNDLE 16
 #endif
@@ -268,10 +271,21 @@ struct TreeRun {
       for (int l = 0; l < 4; ++l) jl[4 * n + l] = j2 + (l >> 1) * RP1 + (l & 1) * RP0;
     }
 #pragma unroll
+#if RQMC_S2_FIRST
+    // all K = 4 nodes' DMMAs issue first: node n+1's tensor work overlaps node n's DFMA work
+    double S2a[NN][NV];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) tree_step<4, NFR, T::XP>(xs(I2, jl[4 * n]), as(I2), c, Sp, S2a[n]);
+#endif
+#pragma unroll
     for (int n = 0; n < NN; ++n) {
       const int j2 = jl[4 * n];
+#if RQMC_S2_FIRST
+      const double (&S2)[NV] = S2a[n];
+#else
       double S2[NV];
       tree_step<4, NFR, T::XP>(xs(I2, j2), as(I2), c, Sp, S2);
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double S1[NV];
