@@ -35,8 +35,14 @@ namespace rqmc {
 // Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36
 // doubles (bank-conflict-free fragment loads); columns >= tau are zero in the A slab and root tile.
 // ------------------------------------------------------------------------------------------
-#ifndef RQMC_S2_FIRST           // bottom block: both K = 4 nodes' DMMAs before the DFMA work (17.02 vs
-#define RQMC_S2_FIRST 1         // 17.34 ms on C5); computing both children of the level above first: slower
+// bottom-block instruction order (C5 fine kernel): both K = 2 tiles of a node before its leaves
+// (S1_FIRST) 16.97 ms; both K = 4 nodes' DMMAs first (S2_FIRST) 17.02; both 17.32; neither 17.34;
+// computing both children of the level above the bottom first: 17.29
+#ifndef RQMC_S2_FIRST
+#define RQMC_S2_FIRST 0
+#endif
+#ifndef RQMC_S1_FIRST
+#define RQMC_S1_FIRST 1
 #endif
 #ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
 #define RQMC_TREE_BUNDLE 16
@@ -286,10 +292,19 @@ struct TreeRun {
       double S2[NV];
       tree_step<4, NFR, T::XP>(xs(I2, j2), as(I2), c, Sp, S2);
 #endif
+#if RQMC_S1_FIRST
+      double S1a[2][NV];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) step_k2(S2, I1, j2 + h * RP1, S1a[h]);
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+#if RQMC_S1_FIRST
+        const double (&S1)[NV] = S1a[h];
+#else
         double S1[NV];
         step_k2(S2, I1, j2 + h * RP1, S1);
+#endif
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int l = 4 * n + 2 * h + q;
