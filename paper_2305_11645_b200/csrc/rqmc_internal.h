@@ -80,7 +80,7 @@ cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, 
                           double* vals, cudaStream_t st);
 cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st);
 // nparts: partial sums written per replica (the tree kernel's bundles may be smaller than kBundle;
-// the workspace holds 2 nbundles partials per replica)
+// the workspace holds 4 nbundles partials per replica)
 cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, int nrep, cudaStream_t st, int64_t* nparts);
 cudaError_t launch_reduce(const double* partial, int64_t n, int64_t stride, int nrep, double* out, cudaStream_t st);
 

@@ -204,7 +204,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   }
   L.off_r[0] = off; off = align_up(off + rsz[0], 256);
   L.off_r[1] = off; off = align_up(off + rsz[1], 256);
-  L.off_part = off; off = align_up(off + (size_t)2 * L.nbundles * sizeof(double), 256);  // see launch_fine
+  L.off_part = off; off = align_up(off + (size_t)4 * L.nbundles * sizeof(double), 256);  // see launch_fine
   L.off_fsum = off; off = align_up(off + sizeof(double), 256);
   L.off_a = off; off = align_up(off + (size_t)p.s * L.ldr * sizeof(double), 256);
   L.total = off;

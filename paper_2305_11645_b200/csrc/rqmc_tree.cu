@@ -61,7 +61,7 @@ struct Tree {
   static constexpr int CH = 4 / NFR;                               // column slices per group
   static constexpr int RWN = BUN / 8;                              // row warps (8 residues each)
   static constexpr int WARPS = 2 * CH * RWN;
-  static constexpr int XP = BUN == 16 ? 20 : kPad;                 // X^red t-stride (conflict-free)
+  static constexpr int XP = BUN == 8 ? 12 : (BUN == 16 ? 20 : kPad);  // X^red t-stride (conflict-free)
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int NV = 2 * NFR;                               // doubles per lane per node
   static constexpr int LEAVES = ipow(B, NF);
@@ -543,9 +543,14 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   }
 }
 
+// residues per CTA (8-residue bundles for the small b = 3 trees, to even out C4's last wave of 1231
+// CTAs, measured slower: fine 3.97 vs 3.83 ms)
+template <int NF, int B>
+constexpr int tree_bundle() { return RQMC_TREE_BUNDLE; }
+
 template <int NF, int B, int G, bool STY>
 static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
-  constexpr int NFR = RQMC_TREE_NFR, BUN = RQMC_TREE_BUNDLE;
+  constexpr int NFR = RQMC_TREE_NFR, BUN = tree_bundle<NF, B>();
   using T = Tree<NF, B, NFR, BUN>;
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
@@ -553,7 +558,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN>, T::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
-  if (nbt > 2 * nb) return cudaErrorInvalidValue;   // workspace holds 2 nb partials per replica
+  if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
   k_fine_tree<NF, B, G, STY, NFR, BUN><<<dim3((unsigned)nbt, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
@@ -562,7 +567,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
 template <int NF, int B>
 static bool tree_matches(const FineArgs& a) {
-  using T = Tree<NF, B, RQMC_TREE_NFR, RQMC_TREE_BUNDLE>;
+  using T = Tree<NF, B, RQMC_TREE_NFR, tree_bundle<NF, B>()>;
   if (a.NF != NF) return false;
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
