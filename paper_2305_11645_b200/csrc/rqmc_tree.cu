@@ -44,6 +44,9 @@ namespace rqmc {
 #ifndef RQMC_S1_FIRST
 #define RQMC_S1_FIRST 1
 #endif
+#ifndef RQMC_TREE_WIDE
+#define RQMC_TREE_WIDE 0
+#endif
 #ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
 #define RQMC_TREE_BUNDLE 16
 #endif
@@ -51,7 +54,7 @@ namespace rqmc {
 #define RQMC_TREE_NFR 4
 #endif
 
-template <int NF, int B, int NFR, int BUN>
+template <int NF, int B, int NFR, int BUN, int NH>
 struct Tree {
   __host__ __device__ static constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
   __host__ __device__ static constexpr int K(int i) { return (B - 1) * ipow(B, NF - 1 - i); }  // s_w, w = NF-1-i
@@ -60,15 +63,19 @@ struct Tree {
   static constexpr int J = ipow(B, NF) - 1;                        // fine A rows
   static constexpr int CH = 4 / NFR;                               // column slices per group
   static constexpr int RWN = BUN / 8;                              // row warps (8 residues each)
-  static constexpr int WARPS = 2 * CH * RWN;
+  static constexpr int NGRP = B;                                   // warp groups: one per top-level run
+  static constexpr int WARPS = NGRP * CH * RWN;
+  static constexpr int MINB = (8 + WARPS - 1) / WARPS;             // CTAs per SM for >= 8 warps
   static constexpr int XP = BUN == 8 ? 12 : (BUN == 16 ? 20 : kPad);  // X^red t-stride (conflict-free)
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int NV = 2 * NFR;                               // doubles per lane per node
   static constexpr int LEAVES = ipow(B, NF);
   static constexpr bool kRegAcc = (B == 2 && NF >= 3);             // register row sums (b = 2 bottom)
-  static constexpr int ABUF = J * kPad;                            // one A slab
+  static constexpr int CW = 32 * NH;                               // CTA column tile (NH passes of 32)
+  static constexpr int AP = CW + 4;                                // A slab / root tile pitch
+  static constexpr int ABUF = J * AP;                              // one A slab
   static constexpr int ROOT = 2 * ABUF;                            // root tiles
-  static constexpr int XS = ROOT + 2 * BUN * kPad;                 // X subtree
+  static constexpr int XS = ROOT + 2 * BUN * AP;                   // X subtree
   static constexpr int XL = (B - 1) * ipow(B, NF) * XP;            // X per level
   static constexpr int ACC = XS + NF * XL;                         // rowacc [ch][leaf][t]
   static constexpr int ACCN = kRegAcc ? 0 : CH * LEAVES * BUN;
@@ -82,7 +89,7 @@ struct TreeCtx {
 };
 
 // S = Sp + X^red[run] A_w, compile-time K (DMMA k-steps of 4, DFMA remainder); xs, as: level bases.
-template <int K, int NFR, int XP>
+template <int K, int NFR, int XP, int AP>
 __device__ __forceinline__ void tree_step(const double* xs, const double* as, const TreeCtx& c,
                                           const double (&Sp)[2 * NFR], double (&S)[2 * NFR]) {
   static_assert(K >= 1, "");
@@ -91,7 +98,7 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
     const double* ab = as + c.cw + c.g;
     double af = xs[c.tg * XP], bf[NFR];
 #pragma unroll
-    for (int cf = 0; cf < NFR; ++cf) bf[cf] = ab[c.tg * kPad + cf * 8];
+    for (int cf = 0; cf < NFR; ++cf) bf[cf] = ab[c.tg * AP + cf * 8];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {  // fragments of step s+1 are loaded before step s's DMMAs issue
       double afn = 0.0, bfn[NFR];
@@ -100,7 +107,7 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
       if (s + 1 < NS) {
         afn = xs[(4 * (s + 1) + c.tg) * XP];
 #pragma unroll
-        for (int cf = 0; cf < NFR; ++cf) bfn[cf] = ab[(4 * (s + 1) + c.tg) * kPad + cf * 8];
+        for (int cf = 0; cf < NFR; ++cf) bfn[cf] = ab[(4 * (s + 1) + c.tg) * AP + cf * 8];
       }
 #pragma unroll
       for (int cf = 0; cf < NFR; ++cf) {
@@ -117,7 +124,7 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
     const double x = xs[kk * XP];
 #pragma unroll
     for (int cf = 0; cf < NFR; ++cf) {
-      const double2 p = *reinterpret_cast<const double2*>(as + kk * kPad + c.cw + cf * 8 + 2 * c.tg);
+      const double2 p = *reinterpret_cast<const double2*>(as + kk * AP + c.cw + cf * 8 + 2 * c.tg);
       if (K < 4 && kk == 0) {
         S[2 * cf] = fma(x, p.x, Sp[2 * cf]);
         S[2 * cf + 1] = fma(x, p.y, Sp[2 * cf + 1]);
@@ -169,9 +176,9 @@ __device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[
   }
 }
 
-template <int NF, int B, int G, bool STY, int NFR, int BUN>
+template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 struct TreeRun {
-  using T = Tree<NF, B, NFR, BUN>;
+  using T = Tree<NF, B, NFR, BUN, NH>;
   static constexpr int NV = T::NV;
   static constexpr bool kB2 = (B == 2 && NF >= 3);
   static constexpr bool kRegAcc = T::kRegAcc && G > 0;
@@ -196,7 +203,7 @@ struct TreeRun {
   __device__ __forceinline__ const double* xs(int i, int j) const {
     return fsm + T::XS + i * T::XL + j * T::K(i) * T::XP + c.t;
   }
-  __device__ __forceinline__ const double* as(int i) const { return c.as + T::jlo(i) * kPad; }
+  __device__ __forceinline__ const double* as(int i) const { return c.as + T::jlo(i) * T::AP; }
 
   // S = Sp + X^red_w[run j] A_w for the K = 2 level (b = 2): cached A values, DFMA
   __device__ __forceinline__ void step_k2(const double (&Sp)[NV], int i, int j, double (&S)[NV]) const {
@@ -207,7 +214,7 @@ struct TreeRun {
   template <int I>
   __device__ __forceinline__ void step(const double (&Sp)[NV], int j, double (&S)[NV]) const {
     if constexpr (B == 2 && T::K(I) == 2) step_k2(Sp, I, j, S);
-    else tree_step<T::K(I), NFR, T::XP>(xs(I, j), as(I), c, Sp, S);
+    else tree_step<T::K(I), NFR, T::XP, T::AP>(xs(I, j), as(I), c, Sp, S);
   }
 
   // leaves of parent run jp (level NF-1), generic shapes: Y store, g sums, smem rowacc[ch][leaf][t]
@@ -234,7 +241,7 @@ struct TreeRun {
           for (int e = 0; e < NV; ++e) Y[e] = fma(x1, a0[KL - 1][e], Y[e]);
         }
       } else {
-        tree_step<KL, NFR, T::XP>(xs(I, j), as(I), c, Sp, Y);
+        tree_step<KL, NFR, T::XP, T::AP>(xs(I, j), as(I), c, Sp, Y);
       }
       tree_store<STY, NFR>(a, Y, j, c);
       if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0);
@@ -281,7 +288,7 @@ struct TreeRun {
     // all K = 4 nodes' DMMAs issue first: node n+1's tensor work overlaps node n's DFMA work
     double S2a[NN][NV];
 #pragma unroll
-    for (int n = 0; n < NN; ++n) tree_step<4, NFR, T::XP>(xs(I2, jl[4 * n]), as(I2), c, Sp, S2a[n]);
+    for (int n = 0; n < NN; ++n) tree_step<4, NFR, T::XP, T::AP>(xs(I2, jl[4 * n]), as(I2), c, Sp, S2a[n]);
 #endif
 #pragma unroll
     for (int n = 0; n < NN; ++n) {
@@ -290,7 +297,7 @@ struct TreeRun {
       const double (&S2)[NV] = S2a[n];
 #else
       double S2[NV];
-      tree_step<4, NFR, T::XP>(xs(I2, j2), as(I2), c, Sp, S2);
+      tree_step<4, NFR, T::XP, T::AP>(xs(I2, j2), as(I2), c, Sp, S2);
 #endif
 #if RQMC_S1_FIRST
       double S1a[2][NV];
@@ -345,7 +352,7 @@ struct TreeRun {
     } else if constexpr (I == NF - 1) {
       leaves(Sp, jp);
     } else if constexpr (I == 0) {
-      for (int q = c.grp; q < B; q += 2) {  // top level split over the two warp groups
+      for (int q = c.grp; q < B; q += T::NGRP) {  // top level: one run per warp group
         double S[NV];
         step<0>(Sp, q, S);
         level<1, 0>(S, q);
@@ -378,20 +385,21 @@ struct TreeRun {
     constexpr int KL = T::K(NF - 1);
     if constexpr (KL <= 2) {
 #pragma unroll
-      for (int q = 0; q < KL; ++q) load_cache(a0[q], as(NF - 1) + q * kPad);
+      for (int q = 0; q < KL; ++q) load_cache(a0[q], as(NF - 1) + q * T::AP);
     }
     if constexpr (K1 == 2) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) load_cache(a1[q], as(NF - 2) + q * kPad);
+      for (int q = 0; q < 2; ++q) load_cache(a1[q], as(NF - 2) + q * T::AP);
     }
     level<0, 0>(Sroot, 0);
   }
 };
 
-template <int NF, int B, int G, bool STY, int NFR, int BUN>
-__global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fine_tree(const FineArgs a) {
-  using T = Tree<NF, B, NFR, BUN>;
-  using Run = TreeRun<NF, B, G, STY, NFR, BUN>;
+template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
+__global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
+    k_fine_tree(const FineArgs a) {
+  using T = Tree<NF, B, NFR, BUN, NH>;
+  using Run = TreeRun<NF, B, G, STY, NFR, BUN, NH>;
   constexpr int NT = T::THREADS, NW = T::WARPS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TreeCtx c;
@@ -427,10 +435,11 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   // column tile operands (cp.async, double buffer): A rows [0, J) x 32 columns and the root tile.
   // (One 256-byte cp.async.bulk per row completing on an mbarrier measured 2.1 ms slower on C5: the
   // 95 small bulk requests per tile serialise in the copy engine.)
-  const int ntiles = (a.tau + kFineBN - 1) / kFineBN;
+  constexpr int CW = T::CW, AP = T::AP;
+  const int ntiles = (a.tau + CW - 1) / CW;
   // fast path (every full tile of a 16-byte-aligned A and root, full bundle): each thread's chunks are
   // fixed rows / columns, so addresses are base + compile-time multiples of a runtime stride
-  constexpr int CPR = kFineBN / 2;                          // 16-byte chunks per row
+  constexpr int CPR = CW / 2;                               // 16-byte chunks per row
   constexpr int RPP = NT / CPR;                             // rows per pass of all threads
   constexpr int UA = (T::J + RPP - 1) / RPP, UR = (BUN + RPP - 1) / RPP;
   const bool fast = a.a_vec && root != nullptr && c.beff == BUN && (a.ldroot % 2) == 0 &&
@@ -438,44 +447,44 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   const int fq = tid / CPR, fcc = (tid % CPR) * 2;
   const double* fa = a.A + (int64_t)fq * a.lda + fcc;
   const double* fr = root ? root + (c.r0 + fq) * a.ldroot + fcc : nullptr;
-  const int fo = fq * kPad + fcc;
+  const int fo = fq * AP + fcc;
   auto load_tile = [&](int buf, int c0) {
     double* as = fsm + buf * T::ABUF;
-    double* rs = fsm + T::ROOT + buf * (BUN * kPad);
-    if (fast && c0 + kFineBN <= a.tau) {
+    double* rs = fsm + T::ROOT + buf * (BUN * AP);
+    if (fast && c0 + CW <= a.tau) {
 #pragma unroll
       for (int u = 0; u < UA; ++u)
         if (u + 1 < UA || fq + u * RPP < T::J)
-          cp_async16(as + fo + u * RPP * kPad, fa + (int64_t)u * RPP * a.lda + c0, true);
+          cp_async16(as + fo + u * RPP * AP, fa + (int64_t)u * RPP * a.lda + c0, true);
 #pragma unroll
       for (int u = 0; u < UR; ++u)
         if (u + 1 < UR || fq + u * RPP < BUN)
-          cp_async16(rs + fo + u * RPP * kPad, fr + (int64_t)u * RPP * a.ldroot + c0, true);
+          cp_async16(rs + fo + u * RPP * AP, fr + (int64_t)u * RPP * a.ldroot + c0, true);
       cp_async_commit();
       return;
     }
     if (a.a_vec) {
-      for (int e = tid; e < T::J * (kFineBN / 2); e += NT) {
-        const int q = e >> 4, cc = (e & 15) * 2;
+      for (int e = tid; e < T::J * CPR; e += NT) {
+        const int q = e / CPR, cc = (e % CPR) * 2;
         const bool ok = c0 + cc < a.tau;
-        cp_async16(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
+        cp_async16(as + q * AP + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     } else {
-      for (int e = tid; e < T::J * kFineBN; e += NT) {
-        const int q = e >> 5, cc = e & 31;
+      for (int e = tid; e < T::J * CW; e += NT) {
+        const int q = e / CW, cc = e % CW;
         const bool ok = c0 + cc < a.tau;
-        cp_async8(as + q * kPad + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
+        cp_async8(as + q * AP + cc, ok ? a.A + (int64_t)q * a.lda + c0 + cc : a.A, ok);
       }
     }
-    for (int e = tid; e < BUN * (kFineBN / 2); e += NT) {
-      const int t = e >> 4, cc = (e & 15) * 2;
+    for (int e = tid; e < BUN * CPR; e += NT) {
+      const int t = e / CPR, cc = (e % CPR) * 2;
       const bool row_ok = root != nullptr && t < c.beff;
       const double* src = root + (c.r0 + t) * a.ldroot + c0 + cc;
       if (c0 + cc + 1 < a.tau || !row_ok) {
-        cp_async16(rs + t * kPad + cc, row_ok ? src : a.A, row_ok);
+        cp_async16(rs + t * AP + cc, row_ok ? src : a.A, row_ok);
       } else {
-        cp_async8(rs + t * kPad + cc, row_ok && c0 + cc < a.tau ? src : a.A, row_ok && c0 + cc < a.tau);
-        cp_async8(rs + t * kPad + cc + 1, a.A, false);
+        cp_async8(rs + t * AP + cc, row_ok && c0 + cc < a.tau ? src : a.A, row_ok && c0 + cc < a.tau);
+        cp_async8(rs + t * AP + cc + 1, a.A, false);
       }
     }
     cp_async_commit();
@@ -485,27 +494,32 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   load_tile(0, 0);
   cp_async_wait<0>();  // X^red subtree and tile 0 resident
   __syncthreads();
+  const int cw0 = c.cw;
   for (int ct = 0; ct < ntiles; ++ct) {
-    c.c0 = ct * kFineBN;
+    c.c0 = ct * CW;
     c.as = fsm + (ct & 1) * T::ABUF;
-    if (ct + 1 < ntiles) load_tile((ct + 1) & 1, (ct + 1) * kFineBN);  // buffer freed by the last barrier
-    double Sroot[T::NV];
-    run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (BUN * kPad) + c.t * kPad);
-    run.tile(Sroot);
+    if (ct + 1 < ntiles) load_tile((ct + 1) & 1, (ct + 1) * CW);  // buffer freed by the last barrier
+#pragma unroll 1
+    for (int h = 0; h < NH; ++h) {   // NH passes of 32 columns per barrier interval
+      c.cw = cw0 + 32 * h;
+      double Sroot[T::NV];
+      run.load_cache(Sroot, fsm + T::ROOT + (ct & 1) * (BUN * AP) + c.t * AP);
+      run.tile(Sroot);
+    }
     cp_async_wait<0>();
     __syncthreads();  // tile ct + 1 landed and visible; buffers (ct & 1) free for tile ct + 2
   }
 
   if constexpr (G > 0) {
     // padded columns (>= tau) hold y = 0 exactly: g(0) = 0 except g = exp, which added exp(0) = 1
-    const double pad = (G == 2) ? (double)(ntiles * kFineBN - a.tau) : 0.0;
+    const double pad = (G == 2) ? (double)(ntiles * CW - a.tau) : 0.0;
     double part = 0.0;
     if constexpr (Run::kRegAcc) {
       // column-slice partial row sums -> complete row sums: slices ch > 0 park theirs in smem (the
       // X region is free after the last tile's barrier), slice 0 adds them in fixed order
       constexpr int NA = Run::NACC;
       double* park = fsm + T::XS + ((c.grp * T::RWN + c.wm) * 32 + lane) * NA;
-      constexpr int PS = 2 * T::RWN * 32 * NA;   // one column slice's parked sums
+      constexpr int PS = T::NGRP * T::RWN * 32 * NA;   // one column slice's parked sums
       if (c.ch > 0) {
 #pragma unroll
         for (int i = 0; i < NA; ++i) park[(c.ch - 1) * PS + i] = run.racc[i];
@@ -543,31 +557,37 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN>::THREADS, 32 / BUN) k_fi
   }
 }
 
-// residues per CTA (8-residue bundles for the small b = 3 trees, to even out C4's last wave of 1231
-// CTAs, measured slower: fine 3.97 vs 3.83 ms)
+// residues per CTA: b = 3 trees run 3 warp groups (one per top-level run; 2 groups split the 3 runs
+// 2:1) of one row warp each, 8-residue bundles, 3+ CTAs per SM
 template <int NF, int B>
-constexpr int tree_bundle() { return RQMC_TREE_BUNDLE; }
+constexpr int tree_bundle() { return B == 3 ? 8 : RQMC_TREE_BUNDLE; }
+// 64-column CTA tiles (two 32-column passes per barrier interval) when the doubled A slab still allows
+// two CTAs per SM: small trees (C4's b = 3, NF = 3) spend their time in per-tile barriers and loads
+template <int NF, int B>
+constexpr int tree_passes() {
+  return (RQMC_TREE_WIDE && Tree<NF, B, RQMC_TREE_NFR, RQMC_TREE_BUNDLE, 2>::SMEM <= 100 * 1024) ? 2 : 1;
+}
 
 template <int NF, int B, int G, bool STY>
 static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
-  constexpr int NFR = RQMC_TREE_NFR, BUN = tree_bundle<NF, B>();
-  using T = Tree<NF, B, NFR, BUN>;
+  constexpr int NFR = RQMC_TREE_NFR, BUN = tree_bundle<NF, B>(), NH = tree_passes<NF, B>();
+  using T = Tree<NF, B, NFR, BUN, NH>;
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
   }
-  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN>, T::SMEM);
+  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
-  k_fine_tree<NF, B, G, STY, NFR, BUN><<<dim3((unsigned)nbt, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
+  k_fine_tree<NF, B, G, STY, NFR, BUN, NH><<<dim3((unsigned)nbt, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
 template <int NF, int B>
 static bool tree_matches(const FineArgs& a) {
-  using T = Tree<NF, B, RQMC_TREE_NFR, tree_bundle<NF, B>()>;
+  using T = Tree<NF, B, RQMC_TREE_NFR, tree_bundle<NF, B>(), 1>;
   if (a.NF != NF) return false;
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
