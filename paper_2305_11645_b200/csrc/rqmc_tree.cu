@@ -45,7 +45,7 @@ namespace rqmc {
 #define RQMC_S1_FIRST 1
 #endif
 #ifndef RQMC_TREE_WIDE
-#define RQMC_TREE_WIDE 0
+#define RQMC_TREE_WIDE 1
 #endif
 #ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
 #define RQMC_TREE_BUNDLE 16
