@@ -315,3 +315,29 @@ def test_coarse_pair_fusion_bit_identical(rq, monkeypatch):
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         res.append(np.load(f))
     assert np.array_equal(res[0], res[1])
+
+
+def test_graph_replay_matches_direct(rq):
+    """Single runs are captured once as a CUDA graph and replayed: replays equal the first (captured)
+    run bit for bit, see in-place changes of A (the graph reads memory at execution), and a profiled
+    run (direct launches) gives the same bits."""
+    prob = W.make_random(61, 2, 12, 120, 96, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    pl = rq.Plan.from_problem(prob)
+    A = dev(prob.A)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    first = float(pl.qn_sum(A, prob.f, prob.fparam, out=out).item())
+    again = float(pl.qn_sum(A, prob.f, prob.fparam, out=out).item())
+    assert first == again
+    pl.profile_enable(1)
+    direct = float(pl.qn_sum(A, prob.f, prob.fparam, out=out).item())
+    pl.profile_enable(0)
+    assert direct == first
+    A.mul_(0.5)                                   # same pointer, new contents
+    half = float(pl.qn_sum(A, prob.f, prob.fparam, out=out).item())
+    prob.A = prob.A * 0.5
+    q = oracle.qn_sum(prob)
+    assert half != first and abs(half - q) <= 1e-12 * abs(q)
+    # xa with Y through the graph path, twice
+    Y1, s1 = pl.xa(A, prob.f, prob.fparam)
+    Y2, s2 = pl.xa(A, prob.f, prob.fparam, Y=Y1.clone())
+    assert torch.equal(Y1, Y2)
