@@ -341,3 +341,36 @@ def test_graph_replay_matches_direct(rq):
     Y1, s1 = pl.xa(A, prob.f, prob.fparam)
     Y2, s2 = pl.xa(A, prob.f, prob.fparam, Y=Y1.clone())
     assert torch.equal(Y1, Y2)
+
+
+def test_graph_cache_many_keys_and_pageable_host(rq):
+    """More distinct argument sets than the graph cache holds (eviction path) all give the direct
+    result; rqmc_qn_host with a pageable (non-pinned) host A equals the device call."""
+    prob = W.make_random(62, 2, 11, 80, 40, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    pl = rq.Plan.from_problem(prob)
+    base = dev(prob.A)
+    pl.profile_enable(1)
+    ref = float(pl.qn_sum(base, prob.f, prob.fparam).item())   # profiled: direct launches
+    pl.profile_enable(0)
+    outs = [torch.empty(1, dtype=torch.float64, device="cuda") for _ in range(11)]
+    for rep in range(2):
+        for o in outs:
+            assert float(pl.qn_sum(base, prob.f, prob.fparam, out=o).item()) == ref
+    h = pl.qn_host(np.array(prob.A, copy=True), prob.f, prob.fparam)   # pageable numpy memory
+    assert h == ref
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_batch_simulated_ranks(rq, G):
+    """Batched shifts under the residue partition: per rank and replica, the partial sums over the
+    G ranks add up to the world = 1 batch result."""
+    prob = W.make_random(70 + G, 2, 12, 60, 40, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    rng = np.random.default_rng(G)
+    shifts = rng.random((5, prob.s))
+    A = dev(prob.A)
+    full = rq.Plan.from_problem(prob).qn_batch(A, prob.f, prob.fparam, shifts=shifts).cpu().numpy()
+    tot = np.zeros(5)
+    for g in range(G):
+        tot += rq.Plan.from_problem(prob, rank=g, world=G).qn_batch(A, prob.f, prob.fparam,
+                                                                     shifts=shifts).cpu().numpy()
+    np.testing.assert_allclose(tot, full, rtol=1e-12)
