@@ -44,6 +44,9 @@ namespace rqmc {
 #ifndef RQMC_S1_FIRST
 #define RQMC_S1_FIRST 1
 #endif
+#ifndef RQMC_CACHE_B4
+#define RQMC_CACHE_B4 1
+#endif
 #ifndef RQMC_TREE_WIDE
 #define RQMC_TREE_WIDE 1
 #endif
@@ -193,6 +196,7 @@ struct TreeRun {
   const TreeCtx& c;
   double a0[T::K(NF - 1) <= 2 ? T::K(NF - 1) : 1][NV];  // leaf A values (K <= 2: DFMA leaves)
   double a1[K1 == 2 ? 2 : 1][NV];                       // A values of the K = 2 level (DFMA)
+  double b4[RQMC_CACHE_B4 && kB2 ? NFR : 1];            // B fragments of the K = 4 level (one DMMA k-step)
   double racc[NACC];                                    // row sums sum_c g(y_kc) of this lane's leaf rows
 
   __device__ __forceinline__ TreeRun(const FineArgs& a_, const TreeCtx& c_) : a(a_), c(c_) {
@@ -258,6 +262,17 @@ struct TreeRun {
     }
   }
 
+  // the K = 4 level of the b = 2 bottom: one DMMA k-step, B fragments cached per tile (RQMC_CACHE_B4)
+  __device__ __forceinline__ void step4(const double* x, const double (&Sp)[NV], double (&S)[NV]) const {
+    if constexpr (RQMC_CACHE_B4 && kB2) {
+      const double af = x[c.tg * T::XP];
+#pragma unroll
+      for (int cf = 0; cf < NFR; ++cf) dmma_c(S[2 * cf], S[2 * cf + 1], af, b4[cf], Sp[2 * cf], Sp[2 * cf + 1]);
+    } else {
+      tree_step<4, NFR, T::XP, T::AP>(x, as(I2), c, Sp, S);
+    }
+  }
+
   // b = 2 bottom (levels K = 4, 2, 1 below the parent tile Sp, bottom block number P of this warp):
   // the NQ level-(NF-3) nodes, their level-(NF-2) tiles and all 4 NQ leaves are formed first; then one
   // transpose-reduce over the 4 lanes of each row leaves lane tg with the column-slice sums of the
@@ -288,7 +303,7 @@ struct TreeRun {
     // all K = 4 nodes' DMMAs issue first: node n+1's tensor work overlaps node n's DFMA work
     double S2a[NN][NV];
 #pragma unroll
-    for (int n = 0; n < NN; ++n) tree_step<4, NFR, T::XP, T::AP>(xs(I2, jl[4 * n]), as(I2), c, Sp, S2a[n]);
+    for (int n = 0; n < NN; ++n) step4(xs(I2, jl[4 * n]), Sp, S2a[n]);
 #endif
 #pragma unroll
     for (int n = 0; n < NN; ++n) {
@@ -297,7 +312,7 @@ struct TreeRun {
       const double (&S2)[NV] = S2a[n];
 #else
       double S2[NV];
-      tree_step<4, NFR, T::XP, T::AP>(xs(I2, j2), as(I2), c, Sp, S2);
+      step4(xs(I2, j2), Sp, S2);
 #endif
 #if RQMC_S1_FIRST
       double S1a[2][NV];
@@ -390,6 +405,10 @@ struct TreeRun {
     if constexpr (K1 == 2) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) load_cache(a1[q], as(NF - 2) + q * T::AP);
+    }
+    if constexpr (RQMC_CACHE_B4 && kB2) {
+#pragma unroll
+      for (int cf = 0; cf < NFR; ++cf) b4[cf] = as(I2)[c.tg * T::AP + c.cw + c.g + cf * 8];
     }
     level<0, 0>(Sroot, 0);
   }
