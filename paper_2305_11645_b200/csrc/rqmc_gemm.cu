@@ -42,7 +42,11 @@ namespace rqmc {
 #ifndef RQMC_GEMM_WMF
 #define RQMC_GEMM_WMF 4
 #endif
-constexpr int kGemmBN = 64, kGemmBK = RQMC_GEMM_BK, kGemmStages = RQMC_GEMM_STAGES;
+#ifndef RQMC_GEMM_BN
+#define RQMC_GEMM_BN 64
+#endif
+constexpr int kGemmBN = RQMC_GEMM_BN, kGemmBK = RQMC_GEMM_BK, kGemmStages = RQMC_GEMM_STAGES;
+constexpr int kGemmWN = kGemmBN / 32;   // warps along N
 
 template <int BM>
 constexpr int gemm_smem_bytes() {
@@ -50,15 +54,15 @@ constexpr int gemm_smem_bytes() {
 }
 
 template <int BM, int CH, int WMF, bool PAIR>
-__global__ void __launch_bounds__(BM / (8 * WMF) * 64) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
+__global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
                                                                    int64_t y0) {
   constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4;
-  constexpr int NT = BM / (8 * WMF) * 64, WR = 8 * WMF;
+  constexpr int NT = BM / (8 * WMF) * 32 * kGemmWN, WR = 8 * WMF;
   extern __shared__ __align__(16) double gsm[];
   double (*Xs)[BM][XS] = reinterpret_cast<double (*)[BM][XS]>(gsm);
   double (*As)[BK][AS] = reinterpret_cast<double (*)[BK][AS]>(gsm + NST * BM * XS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, tg = lane & 3;  // warp grid (BM / WR) x 2
+  const int wm = warp / kGemmWN, wn = warp % kGemmWN, g = lane >> 2, tg = lane & 3;  // warp grid (BM / WR) x WN
   // sibling-first row blocks: rows [rb, rb + BM) of slice u, valid while inside the slice and < M
   const int64_t yb = y0 + blockIdx.y;  // grid.y <= 65535: long levels launch in chunks
   const int64_t pb = yb / nu, u = yb - pb * nu;
@@ -197,7 +201,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
 #else
   constexpr int BM = RQMC_GEMM_BM;
 #endif
-  constexpr int WMF = RQMC_GEMM_WMF, NT = BM / (8 * WMF) * 64;
+  constexpr int WMF = RQMC_GEMM_WMF, NT = BM / (8 * WMF) * 32 * kGemmWN;
   // sibling-first ordering when the parent has at least one full row block; else plain row blocks
   int64_t mp_blk = a.M, nu = 1;
   if (RQMC_GEMM_SIBLING && a.Rp && a.Mp >= BM && a.Mp < a.M) {
