@@ -194,3 +194,29 @@ def test_batch_layout_and_workspace(rq):
     assert pl.summary_batch(1, W.F_EXP_MEAN)["checkpoint"] == one["checkpoint"]
     assert pl.workspace_size_batch(16) >= 16 * pl.workspace_size_batch(1) // 2
     assert pl.workspace_size_batch(16) > pl.workspace_size_batch(1)
+
+
+def test_run_call_validation(rq):
+    """Run-call argument checks of the C ABI return their status before any device work (rqmc.h):
+    workspace below rqmc_workspace_size -> EINVAL, lda/ldy < tau -> EDIM, missing / bad f -> EINVAL,
+    batch shift outside [0,1) -> ESHIFT, unshifted plan for a lattice batch -> EINVAL, bad level ->
+    EINVAL.  Fake non-null pointers are never dereferenced on these paths."""
+    L = rq.lib()
+    p = _plan(rq, shift=[0.1, 0.2, 0.3, 0.4])
+    need = p.workspace_size()
+    fake = C.c_void_p(0x1000)
+    fs = C.c_void_p(0x2000)
+    fp = (C.c_double * 2)(0.2, 1.0)
+    st = C.c_void_p(0)
+    assert L.rqmc_xa(p._h, fake, 3, fake, 3, 0, fp, fs, fake, need - 1, st) == 1        # EINVAL
+    assert L.rqmc_xa(p._h, fake, 2, fake, 3, 0, fp, fs, fake, need, st) == 7            # EDIM (lda)
+    assert L.rqmc_xa(p._h, fake, 3, fake, 2, 0, fp, fs, fake, need, st) == 7            # EDIM (ldy)
+    assert L.rqmc_qn(p._h, fake, 3, -1, fp, fs, fake, need, st) == 1                    # EINVAL (no f)
+    assert L.rqmc_qn(p._h, fake, 3, 9, fp, fs, fake, need, st) == 1                     # EINVAL (bad f)
+    assert L.rqmc_qn(p._h, fake, 3, 1, None, fs, fake, need, st) == 1                   # CALL needs fparam
+    bad = (C.c_double * 8)(*([0.5] * 7 + [1.0]))
+    assert L.rqmc_qn_batch(p._h, 2, bad, None, None, fake, 3, 0, fp, fs, fake, 1 << 30, st) == 5  # ESHIFT
+    q = _plan(rq)                                                                        # unshifted
+    ok = (C.c_double * 8)(*([0.5] * 8))
+    assert L.rqmc_qn_batch(q._h, 2, ok, None, None, fake, 3, 0, fp, fs, fake, 1 << 30, st) == 1   # EINVAL
+    assert L.rqmc_points(p._h, 99, 0, 1, None, None, st) == 1                           # EINVAL (level)
