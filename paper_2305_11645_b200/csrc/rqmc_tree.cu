@@ -47,6 +47,9 @@ namespace rqmc {
 #ifndef RQMC_CACHE_B4
 #define RQMC_CACHE_B4 1
 #endif
+#ifndef RQMC_FAST_EXP
+#define RQMC_FAST_EXP 1
+#endif
 #ifndef RQMC_TREE_WIDE
 #define RQMC_TREE_WIDE 1
 #endif
@@ -139,13 +142,106 @@ __device__ __forceinline__ void tree_step(const double* xs, const double* as, co
   }
 }
 
+// 2^(j/64), j = 0..63, correctly rounded (mpmath): the table of exp_t
+__device__ __constant__ static const double kExp2Tab64[64] = {
+1.0,
+    1.0108892860517005,
+    1.0218971486541166,
+    1.0330248790212284,
+    1.0442737824274138,
+    1.0556451783605572,
+    1.0671404006768237,
+    1.0787607977571199,
+    1.0905077326652577,
+    1.102382583307841,
+    1.1143867425958924,
+    1.1265216186082418,
+    1.1387886347566916,
+    1.1511892299529827,
+    1.1637248587775775,
+    1.1763969916502812,
+    1.189207115002721,
+    1.202156731452703,
+    1.215247359980469,
+    1.22848053610687,
+    1.241857812073484,
+    1.255380757024691,
+    1.2690509571917332,
+    1.2828700160787783,
+    1.2968395546510096,
+    1.3109612115247644,
+    1.3252366431597413,
+    1.339667524053303,
+    1.3542555469368927,
+    1.3690024229745905,
+    1.383909881963832,
+    1.3989796725383112,
+    1.4142135623730951,
+    1.42961333839197,
+    1.4451808069770467,
+    1.460917794180647,
+    1.4768261459394993,
+    1.4929077282912648,
+    1.5091644275934228,
+    1.5255981507445384,
+    1.5422108254079407,
+    1.559004400237837,
+    1.5759808451078865,
+    1.593142151342267,
+    1.6104903319492543,
+    1.6280274218573478,
+    1.645755478153965,
+    1.6636765803267364,
+    1.681792830507429,
+    1.7001063537185235,
+    1.718619298122478,
+    1.7373338352737062,
+    1.7562521603732995,
+    1.7753764925265212,
+    1.7947090750031072,
+    1.8142521755003989,
+    1.8340080864093424,
+    1.8539791250833855,
+    1.8741676341103,
+    1.8945759815869656,
+    1.9152065613971474,
+    1.9360617934922943,
+    1.9571441241754002,
+    1.978456026387951
+};
+
+// exp(x) for the elementwise g = exp(p0 y) of C2 (|x| <= 700, clamped): x = (k/64) ln 2 + r with
+// |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
+// (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
+// exponent field.  11 fp64 instructions + 1 LDS vs 16 fp64 + branch for exp(); <= ~2.5 ulp.
+__device__ __forceinline__ double exp_t(double x, const double* etab) {
+  x = fmin(fmax(x, -700.0), 700.0);
+  const double kd = rint(x * 92.33248261689366);                 // 64 / ln 2
+  double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
+  r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  const double v = etab[k & 63] * p;
+  return __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
+}
+
 // lane-local sum of g over one leaf node's NV values (reading C-17: 1 identity, 2 exp(p0 y), 3 y^2)
 template <int G, int NV>
-__device__ __forceinline__ double gsum(const double (&S)[NV], double p0) {
+__device__ __forceinline__ double gsum(const double (&S)[NV], double p0, const double* etab) {
   if constexpr (G == 2) {
+#if RQMC_FAST_EXP
+    double v = exp_t(p0 * S[0], etab);
+#pragma unroll
+    for (int e = 1; e < NV; ++e) v += exp_t(p0 * S[e], etab);
+#else
     double v = exp(p0 * S[0]);
 #pragma unroll
     for (int e = 1; e < NV; ++e) v += exp(p0 * S[e]);
+#endif
     return v;
   } else if constexpr (G == 3) {
     double v = S[0] * S[0];
@@ -198,6 +294,7 @@ struct TreeRun {
   double a1[K1 == 2 ? 2 : 1][NV];                       // A values of the K = 2 level (DFMA)
   double b4[RQMC_CACHE_B4 && kB2 ? NFR : 1];            // B fragments of the K = 4 level (one DMMA k-step)
   double racc[NACC];                                    // row sums sum_c g(y_kc) of this lane's leaf rows
+  const double* etab = nullptr;                         // g = exp: 2^(j/64) table in shared memory
 
   __device__ __forceinline__ TreeRun(const FineArgs& a_, const TreeCtx& c_) : a(a_), c(c_) {
 #pragma unroll
@@ -248,7 +345,7 @@ struct TreeRun {
         tree_step<KL, NFR, T::XP, T::AP>(xs(I, j), as(I), c, Sp, Y);
       }
       tree_store<STY, NFR>(a, Y, j, c);
-      if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0);
+      if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0, etab);
     }
     if constexpr (G > 0) {
 #pragma unroll
@@ -335,7 +432,7 @@ struct TreeRun {
 #pragma unroll
           for (int e = 0; e < NV; ++e) Y[e] = fma(x0, a0[0][e], S1[e]);
           tree_store<STY, NFR>(a, Y, jl[l], c);
-          if constexpr (G > 0) v[l] = gsum<G, NV>(Y, a.fp0);
+          if constexpr (G > 0) v[l] = gsum<G, NV>(Y, a.fp0, etab);
         }
       }
     }
@@ -510,6 +607,11 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
   };
 
   Run run(a, c);
+  if constexpr (G == 2) {   // exp_t's table, visible after the barrier below
+    __shared__ double etab[64];
+    if (tid < 64) etab[tid] = kExp2Tab64[tid];
+    run.etab = etab;
+  }
   load_tile(0, 0);
   cp_async_wait<0>();  // X^red subtree and tile 0 resident
   __syncthreads();
