@@ -168,9 +168,9 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
  * one replica), ESHIFT (shift outside [0,1) / >= 2^53), ECUDA. */
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes);
 /* The layout a batch of R concurrent replicas with integrand f uses: replicas add parallelism, so
- * the checkpoint may sit coarser (more fused fine levels) than for a single run -- except for
- * f = RQMC_F_CALL_MEAN_EXP (exp-bound, measured slower fused deeper).  Fields checkpoint, n_fine,
- * n_bundles describe the batch layout; the rest as rqmc_plan_summary_get. */
+ * the checkpoint may sit coarser (more fused fine levels) than for a single run.  Fields checkpoint,
+ * n_fine, n_bundles describe the batch layout; the rest as rqmc_plan_summary_get.  (f is reserved:
+ * the current choice does not depend on it.) */
 rqmc_status rqmc_plan_summary_batch(rqmc_plan_t p, int R, int f, rqmc_plan_summary* out);
 rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uint64_t* hdshifts,
                           const uint64_t* hseeds, const double* dA, int64_t lda, rqmc_f f,

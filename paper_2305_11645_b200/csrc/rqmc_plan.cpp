@@ -151,13 +151,16 @@ constexpr int kFineSmemLimit = 200 * 1024;
 
 // Checkpoint choice: the most fused fine levels subject to depth <= kMaxFine, shared memory, and at
 // least 2 waves of fine CTAs (bundles x replicas >= 2 x 148 SMs) -- replicas of a batched run add
-// parallelism, so a batch may fuse more levels than a single run of the same plan.
+// parallelism, so a batch may fuse more levels than a single run of the same plan.  With few column
+// tiles (tau < 1024) a deep subtree's X^red load is amortised over too little work: depth <= 4
+// (C2 x 64 replicas: 2.83 ms fused 4 deep, 4.19 ms 6 deep, 3.61 ms 2 deep).
 int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
   const int nl = (int)p.lv.size();
+  const int max_nf = p.tau < 1024 ? 4 : kMaxFine;
   int best = -1;
   for (int c = 0; c < nl; ++c) {
     const int nf = nl - 1 - c;
-    if (nf > kMaxFine) continue;
+    if (nf > max_nf && c + 1 < nl) continue;
     if (fine_smem_bytes(p, c, nullptr, nullptr, nullptr, nullptr, nullptr) > kFineSmemLimit) continue;
     const int64_t nb = (p.lv[c].Ml + kBundle - 1) / kBundle;
     if (best < 0) best = c;
@@ -224,11 +227,10 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
 }
 
 // Layout for a batch of `reps` concurrent replicas (cached; the single-run layout when equal).
-// g = exp (RQMC_F_CALL_MEAN_EXP) keeps the single-run checkpoint: its fused fine kernel is bound by
-// the N tau exp evaluations and register pressure, and measured slower fused deeper (C2, R = 64:
-// 4.51 ms at checkpoint w = 6 vs 3.98 ms at w = 2).
+// (f is kept for the ABI: the choice no longer depends on it.)
 const Layout& layout_for(rqmc_plan_s* p, int64_t reps, int f) {
-  const int c = choose_ckpt(*p, f == RQMC_F_CALL_MEAN_EXP ? 1 : reps);
+  (void)f;
+  const int c = choose_ckpt(*p, reps);
   if (c == p->L1.ckpt || c < 0) return p->L1;
   std::lock_guard<std::mutex> lk(p->lay_mu);
   for (auto& L : p->lay_cache)
