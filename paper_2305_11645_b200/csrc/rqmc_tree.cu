@@ -14,26 +14,29 @@
 namespace rqmc {
 
 // ------------------------------------------------------------------------------------------
-// k_fine_tree<NF, B, G, STY, NFR>.  Fine level i (coarse -> fine) is w = NF-1-i with
+// k_fine_tree<NF, B, G, STY, NFR, BUN, NH>.  Fine level i (coarse -> fine) is w = NF-1-i with
 // K_i = (B-1) B^{NF-1-i} coordinates, every node has B children, and the fine coordinates are the
 // prefix j < B^NF - 1 of A.  With the whole tree compile-time every loop is unrolled and every
 // smem offset is a constant.
 //
-// CTA = one bundle of 32 checkpoint residues x one 32-column tile at a time (64 tiles for tau =
-// 2048), 2 warp groups (group h walks the subtrees under the top level's runs q = h mod 2) x
-// 4/NFR column slices x 4 row blocks.  A warp owns 8 residues x 8 NFR columns = NFR DMMA.8x8x4
+// CTA = one bundle of BUN checkpoint residues (16; 8 for b = 3) x one CW = 32 NH column tile at a
+// time (NH = 2: two 32-column passes per barrier interval when the doubled A slab still allows two
+// CTAs per SM), B warp groups (group h walks the subtree under the top level's run q = h) x 4/NFR
+// column slices x BUN/8 row warps.  A warp owns 8 residues x 8 NFR columns = NFR DMMA.8x8x4
 // accumulator fragments, so a tree node is 2 NFR doubles per lane and the DFS stack lives in
-// registers.  NFR = 4 (8 warps, 255 registers) is the default; NFR = 2 (16 warps, 128 registers,
-// more LDS and shuffles per output) measured 2 % slower on C5 (20.03 vs 19.59 ms).
+// registers.  NFR = 4 (255 registers, 2 CTAs of 4 warps per SM on C5) is the default; NFR = 2
+// (128 registers, more LDS and shuffles per output) measured 2 % slower.
 //
-//   K >= 4 levels : DMMA.8x8x4 k-steps (mma.sync f64, C and D in distinct registers)
+//   K >= 4 levels : DMMA.8x8x4 k-steps (mma.sync f64, C and D in distinct registers); the K = 4
+//                   level's B fragments cached per tile
 //   K = 2 level   : 2 DFMA per output on A values cached in registers per column tile
-//   K = 1 leaves  : 1 DFMA per output, then Y store / g, lane-local sums of g
+//   K = 1 leaves  : 1 DFMA per output, then Y store / g, lane-local sums of g (g = exp: exp_t)
 //   row sums      : b = 2: one transpose-reduce over the 4 lanes of a row per 4 NQ leaves; each
 //                   lane keeps complete column-slice sums of its leaf rows in registers across all
 //                   column tiles (no shared-memory row accumulators); other shapes: smem rowacc.
-// Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc], t / c strides padded to 36
-// doubles (bank-conflict-free fragment loads); columns >= tau are zero in the A slab and root tile.
+// Shared memory: [A slab x2][root tile x2][X^red subtree][rowacc]; A / root pitch CW + 4, X^red
+// t-stride 20 (BUN 16) / 12 (BUN 8) doubles: bank-conflict-free fragment loads.  Columns >= tau are
+// zero in the A slab and the root tile.
 // ------------------------------------------------------------------------------------------
 // bottom-block instruction order (C5 fine kernel): both K = 2 tiles of a node before its leaves
 // (S1_FIRST) 16.97 ms; both K = 4 nodes' DMMAs first (S2_FIRST) 17.02; both 17.32; neither 17.34;
