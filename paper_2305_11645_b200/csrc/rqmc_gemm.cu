@@ -190,17 +190,26 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
   }
 }
 
+template <int BM>
+static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st);
+
 cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
   if (a.M == 0 || nrep == 0) return cudaSuccess;
+  // 64-row tiles (4 CTAs per SM) everywhere: 32-row tiles for levels under 2 waves (one rank's share
+  // of C5 on 8 GPUs) measured slower (per-rank 4.08 vs 4.04 ms)
+#ifdef RQMC_GEMM_BM
+  return launch_gemm_bm<RQMC_GEMM_BM>(a, nrep, st);
+#else
+  return launch_gemm_bm<64>(a, nrep, st);
+#endif
+}
+
+template <int BM>
+static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) {
   const bool pair = a.Xc != nullptr;
   const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
                    (!pair || ((uintptr_t)a.Ac % 16 == 0)) &&
                    (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
-#ifndef RQMC_GEMM_BM
-  constexpr int BM = 64;
-#else
-  constexpr int BM = RQMC_GEMM_BM;
-#endif
   constexpr int WMF = RQMC_GEMM_WMF, NT = BM / (8 * WMF) * 32 * kGemmWN;
   // sibling-first ordering when the parent has at least one full row block; else plain row blocks
   int64_t mp_blk = a.M, nu = 1;
