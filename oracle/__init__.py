@@ -10,7 +10,8 @@ the plain definitions of PAPER.md (P:n = line n):
   product Y = X A, naive triple loop in increasing j
   Q_N     N^-1 sum_k f(x_k^T A) with Neumaier summation
 Every function is pinned by tests/test_oracle_pins.py.
-Parity unpinned: f_rows for f = CALL_MEAN_EXP (C2) and MEAN_SQ (C4) beyond the naive definition.
+f = MEAN_SQ (C4) is pinned by an exact-rational brute force of Q_N, f = CALL_MEAN_EXP (C2) by a
+40-digit mpmath evaluation of the definition on exact rational points (tests/test_oracle_pins.py).
 """
 from __future__ import annotations
 

@@ -382,3 +382,56 @@ def test_meanid_tabulated_equals_rowwise():
         tab = oracle.f_all_meanid_tab(prob)
         assert np.array_equal(tab, oracle.f_rows_meanid(prob, ks))
         np.testing.assert_allclose(tab, oracle.f_rows(prob, ks), rtol=1e-13)
+
+
+# ---------------------------------------------------------------- Q_N for the C2 / C4 integrands
+
+def _exact_points(b, m, w, z, shift):
+    """x_{k,j} = {k z_j / N + Delta_j} in exact rationals, z_j = b^{w_j} z'_j."""
+    N = b ** m
+    pts = []
+    for k in range(N):
+        row = []
+        for j in range(len(w)):
+            zj = (b ** min(w[j], m)) * z[j] % N if w[j] < m else 0
+            x = Fr(k * zj % N, N) + Fr(shift[j])
+            row.append(x - 1 if x >= 1 else x)
+        pts.append(row)
+    return pts
+
+
+def test_qn_mean_sq_exact_rational():
+    """C4's f = mean(y^2) (reading C-17): the oracle's Q_N sum over a b = 3 shifted lattice with an
+    integer A equals the exact rational sum of the definition (brute force) to 1e-15."""
+    b, m, w, z = 3, 3, [0, 0, 1, 2], [1, 2, 4, 1]
+    shift = [Fr(1, 8), Fr(3, 4), Fr(0), Fr(5, 16)]   # dyadic shifts: exact in fp64
+    A = np.array([[1, -2, 3], [2, 0, -1], [-1, 1, 1], [3, 2, -2]], dtype=np.float64)
+    p = W.Problem("t", W.KIND_LATTICE, b, m, 4, 3, np.array(w, np.int32), np.array(z, np.uint64), None,
+                  np.array([float(s) for s in shift]), None, W.MAP_UNIT, A, W.F_MEAN_SQ, np.zeros(2), True, 0)
+    exact = Fr(0)
+    for x in _exact_points(b, m, w, z, shift):
+        y = [sum(x[j] * int(A[j, c]) for j in range(4)) for c in range(3)]
+        exact += sum(v * v for v in y) / 3
+    q = oracle.qn_sum(p)
+    assert abs(q - float(exact)) <= 1e-15 * float(exact)
+
+
+def test_qn_call_mean_exp_high_precision():
+    """C2's f = max(mean exp(0.2 y) - 1, 0) (reading C-17): the oracle's Q_N sum over a b = 2 shifted
+    lattice equals the definition evaluated on the exact rational points in 40-digit arithmetic
+    (mpmath, an exp implementation independent of libm) to 1e-14 relative."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    b, m, w, z = 2, 5, [0, 1, 1, 2, 3], [3, 1, 5, 3, 1]
+    shift = [Fr(1, 32), Fr(7, 16), Fr(3, 8), Fr(0), Fr(9, 64)]
+    A = np.array([[2.5, -1.0], [1.0, 3.0], [-2.0, 0.5], [4.0, 1.5], [0.25, -3.0]])
+    p = W.Problem("t", W.KIND_LATTICE, b, m, 5, 2, np.array(w, np.int32), np.array(z, np.uint64), None,
+                  np.array([float(s) for s in shift]), None, W.MAP_UNIT, A, W.F_CALL_MEAN_EXP,
+                  np.array([0.2, 1.0]), True, 0)
+    ref = mp.mpf(0)
+    Am = [[mp.mpf(float(v)) for v in row] for row in A]
+    for x in _exact_points(b, m, w, z, shift):
+        y = [mp.fsum(mp.mpf(x[j].numerator) / x[j].denominator * Am[j][c] for j in range(5)) for c in range(2)]
+        ref += max(mp.fsum(mp.exp(mp.mpf("0.2") * v) for v in y) / 2 - 1, 0)
+    q = oracle.qn_sum(p)
+    assert abs(q - float(ref)) <= 1e-14 * float(ref)
