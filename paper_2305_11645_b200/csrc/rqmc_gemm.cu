@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
   const int wm = warp / kGemmWN, wn = warp % kGemmWN, g = lane >> 2, tg = lane & 3;  // warp grid (BM / WR) x WN
   // sibling-first row blocks: rows [rb, rb + BM) of slice u, valid while inside the slice and < M
   const int64_t yb = y0 + blockIdx.y;  // grid.y <= 65535: long levels launch in chunks
-  const int64_t pb = yb / nu, u = yb - pb * nu;
+  const int64_t pb = (int64_t)((uint32_t)yb / (uint32_t)nu), u = yb - pb * nu;  // 32-bit: yb < 2^31, nu small
   const int64_t in0 = pb * BM;                       // offset inside the slice
   const int64_t r0 = u * mp_blk + in0;               // first row of the tile
   const int64_t rlim = min(a.M, u * mp_blk + mp_blk);  // rows >= rlim belong to another tile
@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
       acc[i][jn][0] = 0.0;
       acc[i][jn][1] = 0.0;
       if (Rpg && row < rlim) {  // tile(R_w'): row r reads parent row r mod M_w'
-        const double* p = Rpg + (row % a.Mp) * a.ldp + col;
+        // sibling-first tiles (mp_blk = Mp) lie inside one period: r mod Mp = in0 + (r - r0)
+        const int64_t prow = (mp_blk == a.Mp) ? in0 + (row - r0) : row % a.Mp;
+        const double* p = Rpg + prow * a.ldp + col;
         if (CH == 2 && col + 1 < a.tau) {
           const double2 v = *reinterpret_cast<const double2*>(p);
           acc[i][jn][0] = v.x;
