@@ -36,7 +36,8 @@ FP64_PEAK_DERIVED = 148 * 128 * 1.965e9      # SMs x fp64 flop/clk/SM x max SM c
 
 
 def describe(prob) -> str:
-    kind = {W.KIND_LATTICE: "lattice", W.KIND_NET: "digital net", W.KIND_MC: "reduced MC"}[prob.kind]
+    kind = {W.KIND_LATTICE: "lattice", W.KIND_NET: "digital net", W.KIND_MC: "reduced MC",
+            W.KIND_NET_ROWS: "row-zeroed digital net (Alg. 4)"}[prob.kind]
     sh = "shift" if (prob.shift is not None or prob.dshift is not None) else "no shift"
     mp = "Phi^-1" if prob.map == W.MAP_INVNORM else "unit cube"
     fn = {0: "exp(mean)", 1: "max(mean(exp(0.2y))-1,0)", 2: "mean(y^2)", 3: "mean(y)"}[prob.f]
@@ -198,7 +199,7 @@ def main():
     if R > 1:   # R independent randomisations of the same plan
         if prob.kind == W.KIND_LATTICE:
             rkw = {"shifts": W.uniform53(prob.seed, 77, R * prob.s).reshape(R, prob.s)}
-        elif prob.kind == W.KIND_NET:
+        elif prob.kind in (W.KIND_NET, W.KIND_NET_ROWS):
             rkw = {"dshifts": (W.stream(prob.seed, 77, R * prob.s) >> np.uint64(11)).reshape(R, prob.s)}
         else:
             rkw = {"seeds": W.stream(prob.seed, 77, R)}

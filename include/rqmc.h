@@ -25,7 +25,8 @@
  *  - Layouts: A row-major s x tau, row j = a_j, leading dimension lda >= tau (elements).
  *    Y row-major (N/world) x tau, ldy >= tau; local row i is global point k = rank + world * i
  *    (residue-class partition, multi-GPU; world = 1 gives Y = XA).
- *  - Point kinds: RQMC_LATTICE, RQMC_DIGITAL_NET (b = 2) and RQMC_REDUCED_MC (see rqmc_kind).
+ *  - Point kinds: RQMC_LATTICE, RQMC_DIGITAL_NET (b = 2), RQMC_REDUCED_MC and
+ *    RQMC_DIGITAL_NET_ROWS (row-zeroed nets, Alg. 4) (see rqmc_kind).
  *  - Precision: fp64 throughout.  Point indices/digits are exact integers; lattice values are
  *    u = t/M (IEEE divide), shift u = u + Delta, if u >= 1 then u - 1 (no FMA contraction).
  *  - Limits: N = b^m <= 2^32; m <= 53 for nets; world must be a power of b dividing N.
@@ -67,7 +68,17 @@ typedef enum {
  *   word  = mix64(key_j + (r+1) * G) >> 11,  u = (word | 1) 2^-53   (exact, odd multiple of
  *   2^-53, so 0 < u < 1 and Phi^-1(u) is finite).
  * The same tree of levels, GEMMs and fused fine kernel computes the product. */
-typedef enum { RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1, RQMC_REDUCED_MC = 2 } rqmc_kind;
+/* RQMC_DIGITAL_NET_ROWS: the paper's own reduced digital net (Alg. 3): any generating
+ * matrices C^(j) (b = 2, same column-word format as RQMC_DIGITAL_NET), with the last min(w_j,m) rows
+ * zeroed by the plan (Eq. reduced_genmat_net2) and no column-deletion requirement.  Coordinate j
+ * then takes only 2^{m-w_j} distinct values, but their pattern in n differs per j, so no rows of
+ * the product repeat: Alg. 4 saves multiplications, not additions.  On the
+ * fp64 datapath an add and an FMA cost the same issue slot, so the plan computes the product as one
+ * dense level of N rows and s* coordinates on the DMMA GEMM (N s* tau MACs = Alg. 4's additions).
+ * Points, shifts (dshift), map, f and the multi-GPU partition are as for RQMC_DIGITAL_NET. */
+typedef enum {
+  RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1, RQMC_REDUCED_MC = 2, RQMC_DIGITAL_NET_ROWS = 3
+} rqmc_kind;
 typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1 } rqmc_map;
 
 /* f(y) = F(tau^-1 sum_c g(y_c))  (SURVEY reading C-17)                                    */
@@ -89,7 +100,8 @@ typedef struct {
                                LSB-first).  The plan applies the paper's row zeroing
                                (Eq. reduced_genmat_net2) and requires the result to
                                have columns q >= m - min(w_j,m) zero (column deletion),
-                               which makes coordinate j periodic in k with period 2^{m-w_j}.  */
+                               which makes coordinate j periodic in k with period 2^{m-w_j}
+                               (RQMC_DIGITAL_NET_ROWS: row zeroing only, any C).             */
   const double* shift;      /* lattice random shift Delta_j in [0,1), or NULL        */
   const uint64_t* dshift;   /* net digital shift sigma_j < 2^53: x = ((W << (53-m)) ^ sigma) 2^-53 */
   rqmc_map map;             /* RQMC_MAP_INVNORM: x = Phi^-1(u), u = 0 remapped (reading C-5) */

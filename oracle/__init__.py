@@ -61,6 +61,7 @@ def lib():
         _lib.orc_f_rows_meanid.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, i64p, C.c_int64, dp, C.c_int]
         _lib.orc_points_rows.argtypes = [C.POINTER(_Prob), i64p, C.c_int64, dp, C.c_int]
         _lib.orc_f_all_meanid_tab.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, C.c_int]
+        _lib.orc_alg4_product.argtypes = [C.POINTER(_Prob), dp, C.c_int, dp]
         _lib.orc_mc_bank_index.restype = C.c_uint64
         _lib.orc_mc_bank_index.argtypes = [C.POINTER(_Prob), C.c_uint64, C.c_int]
         _lib.orc_mc_word.restype = C.c_uint64
@@ -192,8 +193,22 @@ def f_all_meanid_tab(prob, nthreads: int = 0) -> np.ndarray:
     fk = np.empty(prob.N)
     err = lib().orc_f_all_meanid_tab(C.byref(h.s), _ptr(A, C.c_double), prob.tau, prob.f, _ptr(fk, C.c_double), nthreads)
     if err:
-        raise ValueError("mean identity needs g = id" if err == 1 else "allocation failed")
+        raise ValueError({1: "mean identity needs g = id", 3: "row-zeroed nets are not periodic"}.get(
+            err, "allocation failed"))
     return fk
+
+
+def alg4_xa(prob) -> np.ndarray:
+    """All N rows of XA by the paper's Alg. 4 for an unshifted, unmapped row-zeroed net
+    (kind 3): a second product path, from the FULL net and the table c_k = (k/b^{m-w_j}) a_j."""
+    h = _Holder(prob)
+    A = np.ascontiguousarray(prob.A, dtype=np.float64)
+    Y = np.empty((prob.N, prob.tau))
+    err = lib().orc_alg4_product(C.byref(h.s), _ptr(A, C.c_double), prob.tau, _ptr(Y, C.c_double))
+    if err:
+        raise ValueError("Alg. 4 needs an unshifted, unmapped row-zeroed net (kind 3)" if err == 1
+                         else "allocation failed")
+    return Y
 
 
 def xa(prob, k0: int = 0, n: int | None = None) -> np.ndarray:

@@ -16,6 +16,7 @@
  *        digital shift (reading C-9): V = (W << (53-m)) XOR sigma_j, x = V 2^-53
  *        reduced MC (Eq. randpts) x_{j,n} = y_{j, m_s N_{s+1} + ... + m_j N_{j+1}} from the
  *                 mixed-radix digits of n; the bank y_{j,r} is the counter-based stream of include/rqmc.h
+ *        row-zeroed net (kind 3): the same definition with any C^(j) (no column deletion assumed)
  *        map      x = Phi^-1(u), zero rule reading C-5
  *   O2 product Y[k,c] = sum_{j=1..s} x_{k,j} A[j,c], increasing j
  *   O3 f_k = F(tau^-1 sum_c g(Y[k,c])) (increasing c); sum_k f_k Neumaier-compensated
@@ -35,7 +36,7 @@
 typedef struct {
   int b, m, s;
   const int32_t* w;        /* s reduction indices, 0 = w_1 <= w_2 <= ... */
-  int kind;                /* 0 lattice, 1 digital net (b = 2) */
+  int kind;                /* 0 lattice, 1 digital net (b = 2), 2 reduced MC, 3 row-zeroed net */
   const uint64_t* z;       /* lattice z'_j */
   const uint64_t* C;       /* net: column words, C[j*m+q] bit (m-1-p) = C^(j)_{p+1,q+1} */
   const double* shift;     /* lattice Delta_j in [0,1) or NULL */
@@ -299,6 +300,7 @@ int orc_f_rows_meanid(const orc_problem* p, const double* A, int tau, int f, con
  * definition at k = 0..M_j-1 and f_k = F(sum_j tab_j[k mod M_j] abar_j) (increasing j). */
 int orc_f_all_meanid_tab(const orc_problem* p, const double* A, int tau, int f, double* fk, int nthreads) {
   if (f != 0 && f != 3) return 1;
+  if (p->kind == 3) return 3;   /* row-zeroed nets are not periodic in k */
   const uint64_t N = ipow((uint64_t)p->b, p->m);
   uint64_t* M = (uint64_t*)malloc(sizeof(uint64_t) * p->s);
   size_t* off = (size_t*)malloc(sizeof(size_t) * (p->s + 1));
@@ -327,5 +329,44 @@ int orc_f_all_meanid_tab(const orc_problem* p, const double* A, int tau, int f, 
     fk[k] = f == 0 ? exp(acc) : acc;
   }
   free(tab); free(M); free(off); free(abar);
+  return 0;
+}
+
+/* Alg. 4, "fast reduced matrix product for digital nets", step by step, for the
+ * unshifted, unmapped row-zeroed net (kind 3).  The input point set is the FULL digital net y_n of
+ * Eq. def:digital (C^(j) without row zeroing); coordinate j uses the table
+ *   c_k = (k / b^{m-w_j}) a_j,  k = 0 .. b^{m-w_j}-1,
+ * and P_j = P_{j+1} + (c_{floor(y_{n,j} b^{m-w_j})})_n, for j = s* down to 1, P_{s*+1} = 0.
+ * Y (N x tau) = P_1.  Returns 1 for shifts / maps / other kinds (Alg. 4 does not define them). */
+int orc_alg4_product(const orc_problem* p, const double* A, int tau, double* Y) {
+  if (p->kind != 3 || p->b != 2 || p->dshift || p->map != 0) return 1;
+  const uint64_t N = ipow(2u, p->m);
+  int s_star = 0;
+  for (int j = 0; j < p->s; ++j)
+    if (p->w[j] < p->m) s_star = j + 1;                       /* s* */
+  for (uint64_t i = 0; i < N * (uint64_t)tau; ++i) Y[i] = 0.0;  /* P_{s*+1} = 0 */
+  double* c = (double*)malloc(sizeof(double) * N * (size_t)tau);
+  if (!c) return 2;
+  for (int j = s_star - 1; j >= 0; --j) {                     /* j = s* .. 1 (0-based) */
+    const uint64_t Mj = ipow(2u, p->m - p->w[j]);               /* b^{m-w_j} */
+    const double* a = A + (size_t)j * tau;
+    for (uint64_t k = 0; k < Mj; ++k)
+      for (int cc = 0; cc < tau; ++cc) c[k * tau + cc] = ((double)k / (double)Mj) * a[cc];
+    for (uint64_t n = 0; n < N; ++n) {
+      /* y_{n,j}: full C^(j) times the digits of n (Eq. def:digital), all m output digits */
+      uint64_t W = 0;
+      for (int pp = 1; pp <= p->m; ++pp) {
+        unsigned y = 0;
+        for (int qq = 1; qq <= p->m; ++qq)
+          y ^= (unsigned)((p->C[(size_t)j * p->m + (qq - 1)] >> (p->m - pp)) & 1u) & (unsigned)((n >> (qq - 1)) & 1u);
+        W |= (uint64_t)y << (p->m - pp);
+      }
+      const double yv = (double)W * ldexp(1.0, -p->m);
+      const uint64_t k = (uint64_t)floor(yv * (double)Mj);     /* floor(y_{n,j} b^{m-w_j}) */
+      double* row = Y + n * (size_t)tau;
+      for (int cc = 0; cc < tau; ++cc) row[cc] = row[cc] + c[k * tau + cc];
+    }
+  }
+  free(c);
   return 0;
 }

@@ -24,7 +24,7 @@ from ._build import LIB as _LIB_PATH
 # A/B experiments only: RQMC_LIB may name another in-tree build (librqmc_<variant>.so)
 _LIB_PATH = os.environ.get("RQMC_LIB", _LIB_PATH)
 
-LATTICE, DIGITAL_NET, REDUCED_MC = 0, 1, 2
+LATTICE, DIGITAL_NET, REDUCED_MC, DIGITAL_NET_ROWS = 0, 1, 2, 3
 MAP_UNIT, MAP_INVNORM = 0, 1
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
 

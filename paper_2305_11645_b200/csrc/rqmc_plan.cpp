@@ -272,11 +272,14 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   if (d->m < 1 || d->s < 1 || d->tau < 1) return bad(RQMC_EDIM, "m, s, tau must be >= 1");
   if (!is_prime(d->b)) return bad(RQMC_ENOTPRIME, "b = " + std::to_string(d->b) + " is not prime");
   if (!d->w) return bad(RQMC_EINVAL, "w is NULL");
-  if (d->kind != RQMC_LATTICE && d->kind != RQMC_DIGITAL_NET && d->kind != RQMC_REDUCED_MC)
+  if (d->kind != RQMC_LATTICE && d->kind != RQMC_DIGITAL_NET && d->kind != RQMC_REDUCED_MC &&
+      d->kind != RQMC_DIGITAL_NET_ROWS)
     return bad(RQMC_EINVAL, "bad kind");
+  // row-zeroed net (Alg. 3/4): the same generator as a net; only the level table differs
+  const bool rowzero = d->kind == RQMC_DIGITAL_NET_ROWS;
   if (d->map != RQMC_MAP_UNIT && d->map != RQMC_MAP_INVNORM) return bad(RQMC_EINVAL, "bad map");
   if (d->m * std::log2((double)d->b) > 32.0 + 1e-9) return bad(RQMC_EUNSUPPORTED, "N = b^m > 2^32");
-  if (d->kind == RQMC_DIGITAL_NET && (d->b != 2 || d->m > 32))
+  if ((d->kind == RQMC_DIGITAL_NET || rowzero) && (d->b != 2 || d->m > 32))
     return bad(RQMC_EUNSUPPORTED, "digital nets need b = 2, m <= 32");
   if (d->w[0] != 0) return bad(RQMC_EWORDER, "w_1 != 0 (P:284)");
   for (int j = 1; j < d->s; ++j)
@@ -284,7 +287,8 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       return bad(RQMC_EWORDER, "w decreases at j = " + std::to_string(j + 1));
 
   auto* p = new rqmc_plan_s();
-  p->b = d->b; p->m = d->m; p->s = d->s; p->tau = d->tau; p->kind = d->kind; p->map = d->map;
+  p->b = d->b; p->m = d->m; p->s = d->s; p->tau = d->tau; p->map = d->map;
+  p->kind = rowzero ? RQMC_DIGITAL_NET : d->kind;
   p->N = ipow(d->b, d->m);
   p->world = d->world <= 0 ? 1 : d->world;
   p->rank = d->rank;
@@ -342,7 +346,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
           return bad(RQMC_ENETMAT, "column word j=" + std::to_string(j + 1) + " q=" + std::to_string(q) + " >= 2^m");
         }
         col &= ~low;  // Eq. reduced_genmat_net2: zero the last min(w_j,m) rows
-        if (q >= d->m - wj && col != 0) {
+        if (!rowzero && q >= d->m - wj && col != 0) {
           delete p;
           return bad(RQMC_ENETMAT, "reduced net coordinate j=" + std::to_string(j + 1) +
                                        " depends on digit " + std::to_string(q) +
@@ -365,10 +369,16 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   {
     std::vector<Level> fine_to_coarse;
     int j = 0;
+    // row-zeroed nets: coordinate j takes 2^{m-w_j} values but with no common period in k
+    // (P:667-669), so every j <= s* sits in one dense level of N rows (w = 0)
+    auto level_of = [&](int jj) {
+      const int wl = std::min<int>(d->w[jj], d->m);
+      return rowzero ? (wl < d->m ? 0 : d->m) : wl;
+    };
     while (j < d->s) {
-      const int wl = std::min<int>(d->w[j], d->m);
+      const int wl = level_of(j);
       int j2 = j;
-      while (j2 < d->s && std::min<int>(d->w[j2], d->m) == wl) ++j2;
+      while (j2 < d->s && level_of(j2) == wl) ++j2;
       // columns j > s* are x = 0: dropped, unless a shift or the map makes them the
       // constant phi_j(Delta_j) / Phi^-1(zero rule) -- then a 1-row level m (reading C-4)
       // (reduced MC: N_j = 1 for w_j >= m -- one i.i.d. draw per coordinate, P:981 N_{s+1} = 1)

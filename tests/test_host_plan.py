@@ -68,6 +68,27 @@ def test_net_validation(rq):
     assert ei.value.name == "ENETMAT"
 
 
+def test_rowzero_net_plan(rq):
+    """RQMC_DIGITAL_NET_ROWS (Alg. 3/4): any C accepted (no column deletion), every
+    coordinate j <= s* in one dense level of N rows, j > s* dropped (unshifted) or the constant level m
+    (shifted); MACs = N s* tau (Alg. 4's additions); b = 3 and words >= 2^m rejected."""
+    m = 4
+    ident = [1 << (m - 1 - q) for q in range(m)]
+    full = [8, 12, 14, 15]
+    p = rq.Plan(2, m, 3, 5, [0, 1, 4], kind=rq.DIGITAL_NET_ROWS, C_words=ident + full + full)
+    assert [(L["w"], L["j_lo"], L["s_w"], L["M"]) for L in p.levels()] == [(0, 0, 2, 16)]
+    assert p.summary()["s_star"] == 2
+    assert p.stats()["macs"] == 16 * 2 * 5
+    p = rq.Plan(2, m, 3, 5, [0, 1, 4], kind=rq.DIGITAL_NET_ROWS, C_words=ident + full + full, dshift=[1, 2, 3])
+    assert [(L["w"], L["j_lo"], L["s_w"], L["M"]) for L in p.levels()] == [(4, 2, 1, 1), (0, 0, 2, 16)]
+    with pytest.raises(rq.RqmcError) as ei:
+        rq.Plan(3, m, 2, 2, [0, 1], kind=rq.DIGITAL_NET_ROWS, C_words=ident + full)
+    assert ei.value.name == "EUNSUPPORTED"
+    with pytest.raises(rq.RqmcError) as ei:
+        rq.Plan(2, m, 2, 2, [0, 1], kind=rq.DIGITAL_NET_ROWS, C_words=ident + [16, 0, 0, 0])
+    assert ei.value.name == "ENETMAT"
+
+
 def test_level_table_tau_I(rq):
     """w = (0,0,1,2,2), m = 3 -> tau_0=2, tau_1=1, tau_2=2."""
     p = rq.Plan(2, 3, 5, 4, [0, 0, 1, 2, 2], z=[1, 3, 1, 1, 1])

@@ -103,8 +103,10 @@ def draw_z(seed: int, b: int, m: int, w: np.ndarray) -> np.ndarray:
     return z
 
 
-def draw_net_matrices(seed: int, m: int, w: np.ndarray) -> np.ndarray:
-    """Unit upper-triangular m x m GF(2) matrices with columns m-w_j..m-1 zeroed (BASELINE C3, reading C-7).
+def draw_net_matrices(seed: int, m: int, w: np.ndarray, delete_cols: bool = True) -> np.ndarray:
+    """Unit upper-triangular m x m GF(2) matrices with columns m-w_j..m-1 zeroed (BASELINE C3, reading C-7);
+    delete_cols=False keeps every column (full nonsingular matrices for the row-zeroed nets of
+    Alg. 3/4, KIND_NET_ROWS, whose row zeroing the plan applies).
 
     Returned as column words: C[j*m + q] holds column q (input digit q, LSB-first digit of n);
     bit (m-1-p) is entry C_{p+1, q+1} (output digit p+1 has weight 2^-(p+1))  (reading C-8).
@@ -113,7 +115,7 @@ def draw_net_matrices(seed: int, m: int, w: np.ndarray) -> np.ndarray:
     u = stream(seed, S_NETC, s * m)
     C = np.zeros(s * m, dtype=np.uint64)
     for j in range(s):
-        keep = m - min(int(w[j]), m)  # columns q < keep survive
+        keep = m - min(int(w[j]), m) if delete_cols else m  # columns q < keep survive
         for q in range(m):
             if q >= keep:
                 continue
@@ -160,7 +162,7 @@ def a_kl(s: int, tau: int) -> np.ndarray:
 
 # f ids (match include/rqmc.h rqmc_f)
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
-KIND_LATTICE, KIND_NET, KIND_MC = 0, 1, 2
+KIND_LATTICE, KIND_NET, KIND_MC, KIND_NET_ROWS = 0, 1, 2, 3
 MAP_UNIT, MAP_INVNORM = 0, 1
 
 
@@ -201,10 +203,16 @@ def as_reduced_mc(prob: Problem, mc_seed: Optional[int] = None) -> Problem:
 
 def make_config(cfg: str, seed: Optional[int] = None) -> Problem:
     """BASELINE.json configs C1..C5 (SURVEY §8(d) 'Inputs (exact)'); a suffix "MC" (e.g. C5MC) gives
-    the same workload with reduced Monte Carlo points (as_reduced_mc)."""
+    the same workload with reduced Monte Carlo points (as_reduced_mc).  "C3R" is C3 with the paper's
+    row-zeroed net (Alg. 3/4): full unit upper-triangular C^(j), the plan zeroes
+    their last w_j rows; same shift, A and f."""
     cfg = cfg.upper()
     if cfg.endswith("MC"):
         return as_reduced_mc(make_config(cfg[:-2], seed))
+    if cfg == "C3R":
+        p = make_config("C3", seed)
+        return dataclasses.replace(p, name="C3R", kind=KIND_NET_ROWS,
+                                   C=draw_net_matrices(p.seed, p.m, p.w, delete_cols=False))
     seeds = {"C1": 1001, "C2": 1002, "C3": 1003, "C4": 1004, "C5": 1005}
     sd = seeds[cfg] if seed is None else seed
     fp = np.zeros(2)
@@ -269,7 +277,7 @@ def make_random(seed: int, b: int, m: int, s: int, tau: int, kind: int = KIND_LA
         return Problem(f"rand{seed}", kind, b, m, s, tau, w, z, None, sh, None, mapping, A, f,
                        np.array([0.2, 1.0]), True, seed)
     assert b == 2
-    C = draw_net_matrices(seed, m, w)
+    C = draw_net_matrices(seed, m, w, delete_cols=kind != KIND_NET_ROWS)
     ds = None
     if shifted:
         ds = stream(seed, S_DSHIFT, s) >> np.uint64(11)
