@@ -164,7 +164,9 @@ int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
     if (fine_smem_bytes(p, c, nullptr, nullptr, nullptr, nullptr, nullptr) > kFineSmemLimit) continue;
     const int64_t nb = (p.lv[c].Ml + kBundle - 1) / kBundle;
     if (best < 0) best = c;
-    if (nb * reps >= 2 * 148) { best = c; break; }
+    // enough bundles (kBundle = 32 residues) for >= 148 16-residue tree CTAs: a finer checkpoint
+    // costs one more GEMM launch, which measured worse than a partial wave (C2: 85.7 vs 90.2 us)
+    if (nb * reps >= 74) { best = c; break; }
     best = c;  // keep moving finer while parallelism is insufficient
   }
   const char* env = std::getenv("RQMC_CKPT_W");        // tuning override: checkpoint at level w

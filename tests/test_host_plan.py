@@ -210,8 +210,10 @@ def test_batch_layout_and_workspace(rq):
     pl = rq.Plan.from_problem(prob)
     one = pl.summary()
     deep = pl.summary_batch(64, W.F_EXP_MEAN)
-    assert deep["n_fine"] > one["n_fine"] and deep["n_bundles"] * 64 >= 2 * 148
+    assert deep["n_fine"] >= one["n_fine"] and deep["n_bundles"] * 64 >= 148
     assert deep["n_fine"] == 4 and pl.summary_batch(64, W.F_CALL_MEAN_EXP) == deep
+    c1 = rq.Plan.from_problem(W.make_config("C1"))   # N = 1024: single runs stay coarse
+    assert c1.summary()["n_fine"] == 0 and c1.summary_batch(64, W.F_EXP_MEAN)["n_fine"] == 4
     assert pl.summary_batch(1, W.F_EXP_MEAN)["checkpoint"] == one["checkpoint"]
     assert pl.workspace_size_batch(16) >= 16 * pl.workspace_size_batch(1) // 2
     assert pl.workspace_size_batch(16) > pl.workspace_size_batch(1)
