@@ -5,11 +5,49 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "rqmc_internal.h"
 
+#ifndef RQMC_PDL
+#define RQMC_PDL 1
+#endif
+
 namespace rqmc {
+
+// Programmatic dependent launch: every kernel of the path is launched with programmatic stream
+// serialisation, so its launch processing and CTA rasterisation overlap the tail of the kernel before
+// it.  Each kernel first waits for its predecessor grid to complete and flush (griddepcontrol.wait:
+// nothing is read or written before), then allows its own successor to launch (its CTAs park at their
+// own wait on slots this grid no longer needs -- all of this grid's CTAs have started by then).
+__device__ __forceinline__ void pdl_enter() {
+#if RQMC_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+#if RQMC_PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+#else
+  k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+#endif
+}
 
 // cudaFuncSetAttribute(max dynamic smem) once per kernel, device and size (a driver call per launch
 // costs microseconds: visible on the small configs C1/C2)

@@ -318,6 +318,7 @@ __device__ __forceinline__ void fine_level(const FineArgs& a, const double (&Sp)
 
 template <int NF, class BT>
 __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
+  pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   FineCtx c;
   c.grp = warp >> 2;
@@ -486,8 +487,7 @@ template <int NF, class BT>
 static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   cudaError_t e = set_smem_once(k_fine<NF, BT>, a.smem_bytes);
   if (e != cudaSuccess) return e;
-  k_fine<NF, BT><<<dim3((unsigned)nb, (unsigned)nrep), kFineThreads, a.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_fine<NF, BT>, dim3((unsigned)nb, (unsigned)nrep), dim3(kFineThreads), a.smem_bytes, st, a);
 }
 
 // Does the bottom of the fine level table match the compile-time shape BT?

@@ -56,6 +56,7 @@ constexpr int gemm_smem_bytes() {
 template <int BM, int CH, int WMF, bool PAIR>
 __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
                                                                    int64_t y0) {
+  pdl_enter();
   constexpr int BN = kGemmBN, BK = kGemmBK, NST = kGemmStages, XS = BK + 4, AS = BN + 4;
   constexpr int NT = BM / (8 * WMF) * 32 * kGemmWN, WR = 8 * WMF;
   extern __shared__ __align__(16) double gsm[];
@@ -228,7 +229,7 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
       dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0),
                 (unsigned)nrep);
-      kern<<<grid, NT, sm, st>>>(a, mp_blk, nu, y0);
+      if (cudaError_t e = launch_k(kern, grid, dim3(NT), sm, st, a, mp_blk, nu, y0)) return e;
     }
     return cudaGetLastError();
   };

@@ -517,6 +517,7 @@ struct TreeRun {
 template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
     k_fine_tree(const FineArgs a) {
+  pdl_enter();
   using T = Tree<NF, B, NFR, BUN, NH>;
   using Run = TreeRun<NF, B, G, STY, NFR, BUN, NH>;
   constexpr int NT = T::THREADS, NW = T::WARPS;
@@ -704,8 +705,8 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
-  k_fine_tree<NF, B, G, STY, NFR, BUN, NH><<<dim3((unsigned)nbt, (unsigned)nrep), T::THREADS, T::SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)nbt, (unsigned)nrep), dim3(T::THREADS),
+                  (size_t)T::SMEM, st, a);
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
