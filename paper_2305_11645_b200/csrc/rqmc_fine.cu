@@ -487,7 +487,7 @@ template <int NF, class BT>
 static cudaError_t launch_fine_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
   cudaError_t e = set_smem_once(k_fine<NF, BT>, a.smem_bytes);
   if (e != cudaSuccess) return e;
-  return launch_k(k_fine<NF, BT>, dim3((unsigned)nb, (unsigned)nrep), dim3(kFineThreads), a.smem_bytes, st, a);
+  return launch_k(k_fine<NF, BT>, dim3((unsigned)nb, (unsigned)nrep), dim3(kFineThreads), a.smem_bytes, st, true, a);
 }
 
 // Does the bottom of the fine level table match the compile-time shape BT?

@@ -229,7 +229,7 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
       dim3 grid((unsigned)((a.tau + kGemmBN - 1) / kGemmBN), (unsigned)std::min<int64_t>(65535, nrb - y0),
                 (unsigned)nrep);
-      if (cudaError_t e = launch_k(kern, grid, dim3(NT), sm, st, a, mp_blk, nu, y0)) return e;
+      if (cudaError_t e = launch_k(kern, grid, dim3(NT), sm, st, true, a, mp_blk, nu, y0)) return e;
     }
     return cudaGetLastError();
   };

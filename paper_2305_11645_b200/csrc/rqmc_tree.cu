@@ -686,16 +686,21 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
 // 2:1) of one row warp each, 8-residue bundles, 3+ CTAs per SM
 template <int NF, int B>
 constexpr int tree_bundle() { return B == 3 ? 8 : RQMC_TREE_BUNDLE; }
+// fragments per warp: b = 3 trees (C4: Y stored, HBM-bound) run 8 warps of 8 x 16 columns at <= 128
+// registers (fine 3.49 -> 3.30 ms); b = 2 trees keep 4 fragments (NFR = 2 measured slower: C3 fine
+// 0.576 -> 0.701 ms, C2 45 -> 49 us)
+template <int NF, int B>
+constexpr int tree_nfr() { return B == 3 ? 2 : RQMC_TREE_NFR; }
 // 64-column CTA tiles (two 32-column passes per barrier interval) when the doubled A slab still allows
 // two CTAs per SM: small trees (C4's b = 3, NF = 3) spend their time in per-tile barriers and loads
 template <int NF, int B>
 constexpr int tree_passes() {
-  return (RQMC_TREE_WIDE && Tree<NF, B, RQMC_TREE_NFR, RQMC_TREE_BUNDLE, 2>::SMEM <= 100 * 1024) ? 2 : 1;
+  return (RQMC_TREE_WIDE && Tree<NF, B, tree_nfr<NF, B>(), RQMC_TREE_BUNDLE, 2>::SMEM <= 100 * 1024) ? 2 : 1;
 }
 
 template <int NF, int B, int G, bool STY>
 static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
-  constexpr int NFR = RQMC_TREE_NFR, BUN = tree_bundle<NF, B>(), NH = tree_passes<NF, B>();
+  constexpr int NFR = tree_nfr<NF, B>(), BUN = tree_bundle<NF, B>(), NH = tree_passes<NF, B>();
   using T = Tree<NF, B, NFR, BUN, NH>;
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
@@ -706,13 +711,13 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
   return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)nbt, (unsigned)nrep), dim3(T::THREADS),
-                  (size_t)T::SMEM, st, a);
+                  (size_t)T::SMEM, st, false, a);
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
 template <int NF, int B>
 static bool tree_matches(const FineArgs& a) {
-  using T = Tree<NF, B, RQMC_TREE_NFR, tree_bundle<NF, B>(), 1>;
+  using T = Tree<NF, B, tree_nfr<NF, B>(), tree_bundle<NF, B>(), 1>;
   if (a.NF != NF) return false;
   for (int i = 0; i < NF; ++i) {
     const FineLevel& L = a.lv[i];
