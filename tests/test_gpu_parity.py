@@ -172,6 +172,42 @@ def test_xa_qn_sweep(rq, seed, b, m, s, tau, kind, shifted, mapping, wmode, f):
     assert abs(fs2 - fs) <= 1e-13 * max(1e-300, abs(fs))
 
 
+@pytest.mark.parametrize("case", ["m1_s1_tau1", "tau1_s200", "s1_tau300", "w_beyond_m", "w_beyond_m_shift",
+                                  "all_zero_w_b5", "A_zero", "rowzero_m1"])
+def test_degenerate_shapes(rq, case):
+    """Degenerate cases of the method: N = b, one coordinate, one column, every w_j >= m for j > 1
+    (s* = 1: zero columns dropped, or constant columns under a shift, reading C-4), the dense product
+    (all w_j = 0), A = 0 (Y = 0, Q_N = F(0) exactly), a 1-digit row-zeroed net."""
+    kw = dict(kind=W.KIND_LATTICE, shifted=False, mapping=W.MAP_UNIT, wmode="log", f=W.F_EXP_MEAN)
+    b, m, s, tau = 2, 1, 1, 1
+    if case == "tau1_s200":
+        b, m, s, tau = 2, 10, 200, 1
+    elif case == "s1_tau300":
+        b, m, s, tau = 3, 6, 1, 300
+    elif case in ("w_beyond_m", "w_beyond_m_shift"):
+        b, m, s, tau = 2, 3, 40, 17
+        kw.update(shifted=case.endswith("shift"), mapping=W.MAP_INVNORM)
+    elif case == "all_zero_w_b5":
+        b, m, s, tau = 5, 3, 30, 20
+        kw.update(wmode="zero", shifted=True)
+    elif case == "A_zero":
+        b, m, s, tau = 2, 9, 50, 33
+        kw.update(shifted=True, mapping=W.MAP_INVNORM)
+    elif case == "rowzero_m1":
+        b, m, s, tau = 2, 1, 6, 5
+        kw.update(kind=W.KIND_NET_ROWS, shifted=True)
+    prob = W.make_random(77, b, m, s, tau, **kw)
+    if case == "A_zero":
+        prob.A[:] = 0.0
+    p, Y, fs = run_xa(rq, prob)
+    if case == "A_zero":
+        assert not Y.any() and fs == float(prob.N)        # exp(mean 0) = 1 per point, exactly
+        return
+    check_y(prob, Y, np.arange(prob.N))
+    fo = oracle.f_rows(prob, np.arange(prob.N))
+    assert abs(fs - oracle.neumaier(fo)) <= 1e-12 * max(1e-300, np.abs(fo).sum())
+
+
 def test_unaligned_lda_path(rq):
     """Odd lda / odd tau (8-byte cp.async path) and a column-sliced A view."""
     prob = W.make_random(55, 2, 10, 40, 67, shifted=True, mapping=W.MAP_INVNORM)

@@ -43,6 +43,7 @@ def _plan(rq, **kw):
     (dict(z=[1, 9, 3, 1]), "EZUNIT"),                          # z'_2 >= b^{m-w_2}
     (dict(shift=[0.0, 1.0, 0.5, 0.5]), "ESHIFT"),
     (dict(m=40), "EUNSUPPORTED"),
+    (dict(m=33), "EUNSUPPORTED"),          # N = 2^33 > 2^32
     (dict(world=3), "EUNSUPPORTED"),
     (dict(s=0, w=[], z=[]), "EDIM"),
 ])
