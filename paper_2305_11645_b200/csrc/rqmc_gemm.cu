@@ -53,7 +53,7 @@ constexpr int gemm_smem_bytes() {
   return (int)sizeof(double) * kGemmStages * (BM * (kGemmBK + 4) + kGemmBK * (kGemmBN + 4));
 }
 
-template <int BM, int CH, int WMF, bool PAIR>
+template <int BM, int CH, int WMF, bool PAIR, bool RAG>
 __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(const GemmArgs a, int64_t mp_blk, int64_t nu,
                                                                    int64_t y0) {
   pdl_enter();
@@ -114,8 +114,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
       if (kt + NST - 1 < nk) load_stage((kt + NST - 1) % NST, (kt + NST - 1) * BK);
       cp_async_commit();
       const int buf = kt % NST;
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
+      auto kstep = [&](int kk) {
         double af[WMF], bf[4];
 #pragma unroll
         for (int i = 0; i < WMF; ++i) af[i] = Xs[buf][wm * WR + i * 8 + g][kk + tg];
@@ -125,6 +124,17 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
         for (int i = 0; i < WMF; ++i)
 #pragma unroll
           for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
+      };
+      // RAG (K % BK != 0): a ragged last tile runs ceil(kl/4) k-steps -- its zero padding would only
+      // add exact zeros (C4's K = 54, 162: 12 %, 7 % of the MACs); compile-time so that the K % BK == 0
+      // levels keep the branch-free loop (C5 coarse 12.35 vs 12.47 ms)
+      const int kl = RAG ? K - kt * BK : BK;
+      if (kl >= BK) {
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) kstep(kk);
+      } else {
+#pragma unroll 1
+        for (int kk = 0; kk < kl; kk += 4) kstep(kk);
       }
     }
     cp_async_wait<0>();
@@ -233,8 +243,10 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     }
     return cudaGetLastError();
   };
-  if (pair) return vec ? go(k_level_gemm<BM, 2, WMF, true>) : go(k_level_gemm<BM, 1, WMF, true>);
-  return vec ? go(k_level_gemm<BM, 2, WMF, false>) : go(k_level_gemm<BM, 1, WMF, false>);
+  if (pair) return vec ? go(k_level_gemm<BM, 2, WMF, true, false>) : go(k_level_gemm<BM, 1, WMF, true, false>);
+  if (a.K % kGemmBK != 0)
+    return vec ? go(k_level_gemm<BM, 2, WMF, false, true>) : go(k_level_gemm<BM, 1, WMF, false, true>);
+  return vec ? go(k_level_gemm<BM, 2, WMF, false, false>) : go(k_level_gemm<BM, 1, WMF, false, false>);
 }
 
 }  // namespace rqmc
