@@ -208,6 +208,22 @@ def test_degenerate_shapes(rq, case):
     assert abs(fs - oracle.neumaier(fo)) <= 1e-12 * max(1e-300, np.abs(fo).sum())
 
 
+def test_qn_host_alternating_inputs(rq):
+    """rqmc_qn_host's A upload runs on a copy stream and the GEMMs wait on its event while every
+    kernel uses programmatic dependent launch: alternating two different host A (8 MB each) call after
+    call must give each A's own result every time (a GEMM that read A before its copy completed
+    would return the other matrix's sum)."""
+    prob = W.make_config("C3")
+    A1 = np.ascontiguousarray(prob.A)
+    A2 = np.ascontiguousarray(prob.A[::-1] * 1.5)
+    pl = rq.Plan.from_problem(prob)
+    ref = [float(pl.qn_sum(dev(A), prob.f, prob.fparam).item()) for A in (A1, A2)]
+    assert abs(ref[0] - ref[1]) > 1e-6 * abs(ref[0])
+    for i in range(24):
+        got = pl.qn_host(A1 if i % 2 == 0 else A2, prob.f, prob.fparam)
+        assert abs(got - ref[i % 2]) <= 1e-13 * abs(ref[i % 2]), (i, got, ref)
+
+
 def test_unaligned_lda_path(rq):
     """Odd lda / odd tau (8-byte cp.async path) and a column-sliced A view."""
     prob = W.make_random(55, 2, 10, 40, 67, shifted=True, mapping=W.MAP_INVNORM)
