@@ -11,6 +11,7 @@ namespace rqmc {
 constexpr int kMaxLevels = 64;
 constexpr int kMaxFine = 8;       // fused fine levels (compile-time DFS depth)
 constexpr int kBundle = 32;       // residues of the checkpoint level per fine CTA
+constexpr int kSplitSlots = 512;  // max tail bundles split over two CTAs (FineArgs::rscr)
 constexpr int kFineBN = 32;       // column tile of the fine kernel
 constexpr int kFinePad = 36;      // padded t / c stride (doubles) of the fine kernel's smem tiles
 constexpr int kFineThreads = 256;
@@ -38,6 +39,7 @@ struct GenArgs {
   int64_t xrep;
   const uint64_t* seeds;
   double* X;                     // workspace base
+  unsigned int* zcnt; int nzcnt; // fine-kernel split counters to zero (replica stride 2 xrep)
   GenLevel lv[kMaxLevels];
 };
 
@@ -73,6 +75,12 @@ struct FineArgs {
   int acc_off;        // rowacc offset (doubles)
   int smem_bytes;
   int64_t xrep, rootrep, partrep;  // replica strides (doubles): X^red, root R, partials (grid.y = replica)
+  // tail split (b = 3 tree kernel): the last bundles of a grid whose final wave would be at most half
+  // full run as two CTAs over half the column tiles each; their per-row g sums meet in rscr and the
+  // second CTA to finish (counter rcnt[slot], zeroed by k_gen) applies F in fixed order (half 0 + 1)
+  double* rscr; int64_t rscr_cap;  // scratch (doubles per replica slice)
+  unsigned int* rcnt; int ncnt;    // counters per replica slice (stride 2 partrep)
+  int64_t nfull; int nsplit;       // set by the launcher
 };
 
 cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, int nrep, cudaStream_t st);

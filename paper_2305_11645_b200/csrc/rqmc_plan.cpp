@@ -41,6 +41,7 @@ struct Layout {
   std::vector<Level> lv;     // copy of the plan's levels with coarse / ldx / xoff / rbuf filled
   int ldr = 0;               // row stride of R buffers
   size_t off_x = 0, off_r[2] = {0, 0}, off_part = 0, off_a = 0, off_fsum = 0, total = 0;
+  size_t off_split = 0, off_cnt = 0; int64_t split_cap = 0;   // fine-kernel tail split (FineArgs::rscr)
   int64_t max_gen_entries = 0;
   int fine_smem = 0, fine_as_stride = 0, fine_acc_off = 0, leafruns = 1;
   std::vector<int> fine_xs_off, fine_as_off;
@@ -223,6 +224,14 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   L.off_r[0] = off; off = align_up(off + rsz[0], 256);
   L.off_r[1] = off; off = align_up(off + rsz[1], 256);
   L.off_part = off; off = align_up(off + (size_t)4 * L.nbundles * sizeof(double), 256);  // see launch_fine
+  {  // tail-split scratch (b = 3 trees): up to kSplitSlots bundles x 2 halves x kBundle b^nfine rows
+    int64_t rows = kBundle;
+    for (int i = 0; i < L.nfine && rows <= (int64_t(1) << 30); ++i) rows *= p.b;
+    const int64_t cap = (int64_t)kSplitSlots * 2 * rows;
+    L.split_cap = (p.b == 3 && L.nfine > 0 && cap * 8 <= (int64_t(64) << 20)) ? cap : 0;
+    L.off_split = off; off = align_up(off + (size_t)L.split_cap * sizeof(double), 256);
+    L.off_cnt = off; off = align_up(off + (L.split_cap ? (size_t)kSplitSlots * sizeof(unsigned int) : 0), 256);
+  }
   L.off_fsum = off; off = align_up(off + sizeof(double), 256);
   L.off_a = off; off = align_up(off + (size_t)p.s * L.ldr * sizeof(double), 256);
   L.total = off;
@@ -538,6 +547,9 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
 
   // a2: reduced points of every level (all replicas: grid.z)
   GenArgs g = gen_args(p, lay, w);
+  if (lay.split_cap) {   // k_gen zeroes the fine kernel's split counters (stream order, every call)
+    g.zcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); g.nzcnt = kSplitSlots;
+  }
   g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
@@ -598,6 +610,10 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   fa.acc_off = lay.fine_acc_off;
   fa.smem_bytes = lay.fine_smem;
   fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
+  if (lay.split_cap) {
+    fa.rscr = reinterpret_cast<double*>(w + lay.off_split); fa.rscr_cap = lay.split_cap;
+    fa.rcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); fa.ncnt = kSplitSlots;
+  }
   int64_t nparts = 0;
   if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st, &nparts), "k_fine")) return s;
   mark(3);

@@ -530,7 +530,21 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
   c.tg = lane & 3;
   c.t = c.wm * 8 + c.g;
   c.cw = c.ch * 8 * NFR;
-  c.r0 = (int64_t)blockIdx.x * BUN;
+  // tail split (b = 3 trees only, FineArgs::nsplit): CTAs past nfull take half a bundle's column tiles
+  // (compile-time off for b = 2: the extra control flow measured 3.5 % slower on C5's fine kernel)
+  constexpr bool kSplit = (B == 3) && (G > 0);
+  int64_t bundle = blockIdx.x;
+  int sidx = 0;
+  bool split = false;
+  if constexpr (kSplit) {
+    split = a.nsplit > 1 && bundle >= a.nfull;
+    if (split) {
+      const int64_t k = bundle - a.nfull;
+      bundle = a.nfull + (k >> 1);
+      sidx = (int)(k & 1);
+    }
+  }
+  c.r0 = bundle * BUN;
   c.beff = (int)((a.Mroot - c.r0) < BUN ? (a.Mroot - c.r0) : BUN);
   const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
   const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
@@ -557,6 +571,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
   // 95 small bulk requests per tile serialise in the copy engine.)
   constexpr int CW = T::CW, AP = T::AP;
   const int ntiles = (a.tau + CW - 1) / CW;
+  const int ct_lo = kSplit && split && sidx ? ntiles / 2 : 0, ct_hi = kSplit && split && !sidx ? ntiles / 2 : ntiles;
   // fast path (every full tile of a 16-byte-aligned A and root, full bundle): each thread's chunks are
   // fixed rows / columns, so addresses are base + compile-time multiples of a runtime stride
   constexpr int CPR = CW / 2;                               // 16-byte chunks per row
@@ -616,14 +631,14 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     if (tid < 64) etab[tid] = kExp2Tab64[tid];
     run.etab = etab;
   }
-  load_tile(0, 0);
-  cp_async_wait<0>();  // X^red subtree and tile 0 resident
+  load_tile(ct_lo & 1, ct_lo * CW);
+  cp_async_wait<0>();  // X^red subtree and the first tile resident
   __syncthreads();
   const int cw0 = c.cw;
-  for (int ct = 0; ct < ntiles; ++ct) {
+  for (int ct = ct_lo; ct < ct_hi; ++ct) {
     c.c0 = ct * CW;
     c.as = fsm + (ct & 1) * T::ABUF;
-    if (ct + 1 < ntiles) load_tile((ct + 1) & 1, (ct + 1) * CW);  // buffer freed by the last barrier
+    if (ct + 1 < ct_hi) load_tile((ct + 1) & 1, (ct + 1) * CW);  // buffer freed by the last barrier
 #pragma unroll 1
     for (int h = 0; h < NH; ++h) {   // NH passes of 32 columns per barrier interval
       c.cw = cw0 + 32 * h;
@@ -639,6 +654,14 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     // padded columns (>= tau) hold y = 0 exactly: g(0) = 0 except g = exp, which added exp(0) = 1
     const double pad = (G == 2) ? (double)(ntiles * CW - a.tau) : 0.0;
     double part = 0.0;
+    // split halves park their complete-over-slices row sums in scratch (row slot idx, same mapping in
+    // both halves); the second half to finish combines them in fixed order (half 0 + half 1)
+    constexpr int SCR = T::LEAVES * BUN;
+    double* scr = (kSplit && split) ? a.rscr + rep * a.partrep + (bundle - a.nfull) * 2 * SCR : nullptr;
+    auto use = [&](int idx, double rs) {
+      if (kSplit && split) scr[sidx * SCR + idx] = rs;
+      else part += f_of_mean(a, (rs - pad) / a.tau);
+    };
     if constexpr (Run::kRegAcc) {
       // column-slice partial row sums -> complete row sums: slices ch > 0 park theirs in smem (the
       // X region is free after the last tile's barrier), slice 0 adds them in fixed order
@@ -656,7 +679,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
           double rs = run.racc[i];
 #pragma unroll
           for (int h = 1; h < T::CH; ++h) rs += park[(h - 1) * PS + i];
-          part += f_of_mean(a, (rs - pad) / a.tau);
+          use(((c.grp * T::RWN + c.wm) * 32 + lane) * NA + i, rs);
         }
       }
     } else {
@@ -666,7 +689,25 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
         double rs = fsm[T::ACC + e];
 #pragma unroll
         for (int h = 1; h < T::CH; ++h) rs += fsm[T::ACC + h * (T::LEAVES * BUN) + e];
-        part += f_of_mean(a, (rs - pad) / a.tau);
+        use(e, rs);
+      }
+    }
+    if constexpr (kSplit) {
+      if (split) {
+        __shared__ int s_last;
+        unsigned int* cnt = a.rcnt + rep * 2 * a.partrep + (bundle - a.nfull);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(cnt, 1u) == 1u;
+        __syncthreads();
+        if (!s_last) return;          // the other half finishes the bundle
+        __threadfence();
+        for (int e = tid; e < T::LEAVES * BUN; e += NT)
+          if (e % BUN < c.beff) {
+            const double rs = __ldcg(scr + e) + __ldcg(scr + SCR + e);
+            part += f_of_mean(a, (rs - pad) / a.tau);
+          }
+        if (tid == 0) *cnt = 0u;      // ready for the next call (k_gen zeroes the counters as well)
       }
     }
 #pragma unroll
@@ -677,7 +718,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t += red[w];
-      a.partial[rep * a.partrep + blockIdx.x] = t;
+      a.partial[rep * a.partrep + bundle] = t;
     }
   }
 }
@@ -710,8 +751,37 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
-  return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)nbt, (unsigned)nrep), dim3(T::THREADS),
-                  (size_t)T::SMEM, st, false, a);
+  // tail split (b = 3): when the last wave would be at most half full, its bundles run as two CTAs over
+  // half the column tiles each (decided from nbt alone, so a replica of a batch sums like a single run)
+  FineArgs b = a;
+  b.nfull = nbt;
+  b.nsplit = 1;
+  if constexpr (B == 3 && G > 0) {
+    static const bool no_split = [] { const char* v = std::getenv("RQMC_NO_SPLIT"); return v && *v && *v != '0'; }();
+    const int ntiles = (a.tau + T::CW - 1) / T::CW;
+    if (!no_split && a.rscr && ntiles >= 2) {
+      static const int64_t slots = [] {
+        int occ = 0, dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::THREADS,
+                                                      T::SMEM);
+        return (int64_t)occ * nsm;
+      }();
+      // RQMC_FORCE_SPLIT=1 (tests): split every bundle, so small problems exercise the combine path
+      const char* fv = std::getenv("RQMC_FORCE_SPLIT");
+      const bool force = fv && *fv && *fv != '0';
+      const int64_t tail = force ? nbt : (slots > 0 && nbt >= slots) ? nbt % slots : 0;
+      if (tail > 0 && (force || 2 * tail <= slots) && tail <= a.ncnt &&
+          tail * 2 * (int64_t)T::LEAVES * BUN <= a.rscr_cap) {
+        b.nfull = nbt - tail;
+        b.nsplit = 2;
+      }
+    }
+  }
+  const int64_t grid = b.nfull + (nbt - b.nfull) * b.nsplit;
+  return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)grid, (unsigned)nrep), dim3(T::THREADS),
+                  (size_t)T::SMEM, st, false, b);
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?

@@ -224,6 +224,26 @@ def test_qn_host_alternating_inputs(rq):
         assert abs(got - ref[i % 2]) <= 1e-13 * abs(ref[i % 2]), (i, got, ref)
 
 
+@pytest.mark.parametrize("seed,m,s,tau,f,shifted", [(61, 11, 100, 40, W.F_MEAN_SQ, True),     # Tree<3, 3>
+                                                   (62, 11, 81, 70, W.F_CALL_MEAN_EXP, True),  # Tree<3, 3>
+                                                   (63, 10, 100, 50, W.F_EXP_MEAN, False)])   # Tree<2, 3>
+def test_b3_tail_split_combine(rq, monkeypatch, seed, m, s, tau, f, shifted):
+    """b = 3 trees split the last, at most half-full wave of bundles over two CTAs by column halves
+    (row sums met in scratch, F applied by the second to finish).  RQMC_FORCE_SPLIT=1 splits every
+    bundle: Y, the fused sum and repeated calls (counters reset) must match the oracle."""
+    monkeypatch.setenv("RQMC_FORCE_SPLIT", "1")
+    prob = W.make_random(seed, 3, m, s, tau, shifted=shifted, mapping=W.MAP_INVNORM, f=f)
+    p, Y, fs = run_xa(rq, prob)
+    check_y(prob, Y, np.arange(prob.N))
+    fo = oracle.f_rows(prob, np.arange(prob.N))
+    q = oracle.neumaier(fo)
+    assert abs(fs - q) <= 1e-12 * max(1e-300, np.abs(fo).sum())
+    A = dev(prob.A)
+    for _ in range(3):
+        fs2 = float(p.qn_sum(A, prob.f, prob.fparam).item())
+        assert abs(fs2 - q) <= 1e-12 * max(1e-300, np.abs(fo).sum())
+
+
 def test_unaligned_lda_path(rq):
     """Odd lda / odd tau (8-byte cp.async path) and a column-sliced A view."""
     prob = W.make_random(55, 2, 10, 40, 67, shifted=True, mapping=W.MAP_INVNORM)
