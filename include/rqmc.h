@@ -142,7 +142,9 @@ int64_t     rqmc_plan_global_row(rqmc_plan_t p, int64_t i);
 rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* local_rows, double* macs, double* min_bytes);
 
 /* Bytes of device workspace a run needs (X^red of every level, checkpoint R buffers, partials,
- * plus a staging copy of A for the *_host entry points). */
+ * b = 3 plans: the fine kernel's tail-split scratch and counters (zeroed by every run itself),
+ * plus a staging copy of A for the *_host entry points).  Contents need no initialisation; one
+ * workspace must not be shared by runs in flight concurrently. */
 rqmc_status rqmc_workspace_size(rqmc_plan_t p, size_t* bytes);
 
 /* Y = X A on this rank's rows (dY non-NULL, ldy >= tau); if f != RQMC_F_NONE and d_fsum != NULL,
