@@ -352,6 +352,29 @@ def test_config_c5_qn_full(rq):
     assert abs(fs - q) <= 1e-12 * abs(q), (fs, q)
 
 
+def test_config_c5_rank_partition(rq):
+    """C5 at full size under the multi-GPU residue partition: for G = 2, 4, 8
+    the ranks' local f-sums add up to the single-GPU sum, and rank g of G = 8 stores its full 34 GB
+    share of Y (rows k = g + 8 i, all 2048 columns): its first 64 rows and 256 seeded rows match the
+    oracle."""
+    prob = W.make_config("C5")
+    A = dev(prob.A)
+    one = float(rq.Plan.from_problem(prob).qn_sum(A, prob.f, prob.fparam).item())
+    for G in (2, 4, 8):
+        tot = sum(float(rq.Plan.from_problem(prob, rank=g, world=G).qn_sum(A, prob.f, prob.fparam).item())
+                  for g in range(G))
+        assert abs(tot - one) <= 1e-12 * abs(one), (G, tot, one)
+    g, G = 5, 8
+    pl = rq.Plan.from_problem(prob, rank=g, world=G)
+    Y, fs = pl.xa(A, prob.f, prob.fparam)
+    rng = np.random.default_rng(11)
+    loc = np.unique(np.concatenate([np.arange(64), rng.integers(0, prob.N // G, 256)])).astype(np.int64)
+    Ys = Y[torch.from_numpy(loc).cuda()].cpu().numpy()
+    del Y
+    torch.cuda.empty_cache()
+    check_y(prob, Ys, g + G * loc)
+
+
 def test_config_c5_panel_rows(rq):
     """C5 points/levels with a 64-column panel of A stored (8.6 GB), sampled rows vs the oracle."""
     prob = W.make_config("C5")
