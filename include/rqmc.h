@@ -190,6 +190,14 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
                           const uint64_t* hseeds, const double* dA, int64_t lda, rqmc_f f,
                           const double* fparam, double* d_fsum, void* dwork, size_t wbytes, void* stream);
 
+/* Inspection / tests (host only, no device needed): the name of the fused fine-level kernel template
+ * a run would launch for a batch of R replicas (R = 1: rqmc_xa / rqmc_qn), integrand f (RQMC_F_NONE:
+ * Y only) and want_y (Y stored or not), e.g. "k_fine_tree<6,2,g=1,Y=0>" (compile-time log_b tree,
+ * NF = 6 fine levels, b = 2, g = identity, Y not stored) or "k_fine<4,BotB2>" (general kernel, 4 fused
+ * levels, hand-scheduled b = 2 bottom block).  Honors RQMC_NO_TREE / RQMC_CKPT_W like the run calls.
+ * Writes a NUL-terminated string of at most len bytes.  Errors: EINVAL (NULL, len 0, R < 1). */
+rqmc_status rqmc_plan_dispatch(rqmc_plan_t p, int R, int f, int want_y, char* buf, size_t len);
+
 /* Debug / parity: the reduced points of level `idx` for local rows [r0, r0+count):
  * d_words[i*s_w+q] = integer word (lattice t = r z'_j mod M; net W or shifted V) and
  * d_vals[i*s_w+q] = the mapped fp64 coordinate.  Either output may be NULL. */

@@ -61,6 +61,7 @@ def lib():
         _lib.orc_f_rows_meanid.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, i64p, C.c_int64, dp, C.c_int]
         _lib.orc_points_rows.argtypes = [C.POINTER(_Prob), i64p, C.c_int64, dp, C.c_int]
         _lib.orc_f_all_meanid_tab.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, C.c_int]
+        _lib.orc_f_all_tab.argtypes = [C.POINTER(_Prob), dp, C.c_int, C.c_int, dp, dp, C.c_int]
         _lib.orc_alg4_product.argtypes = [C.POINTER(_Prob), dp, C.c_int, dp]
         _lib.orc_mc_bank_index.restype = C.c_uint64
         _lib.orc_mc_bank_index.argtypes = [C.POINTER(_Prob), C.c_uint64, C.c_int]
@@ -195,6 +196,20 @@ def f_all_meanid_tab(prob, nthreads: int = 0) -> np.ndarray:
     if err:
         raise ValueError({1: "mean identity needs g = id", 3: "row-zeroed nets are not periodic"}.get(
             err, "allocation failed"))
+    return fk
+
+
+def f_all_tab(prob, f: int | None = None, nthreads: int = 0) -> np.ndarray:
+    """f_k for k = 0..N-1 by O1+O2+O3 with column tabulation and row/column cache blocking (same
+    arithmetic order per entry as f_rows; any f; periodic kinds only)."""
+    h = _Holder(prob)
+    A = np.ascontiguousarray(prob.A, dtype=np.float64)
+    fp = np.ascontiguousarray(np.asarray(prob.fparam, dtype=np.float64))
+    fk = np.empty(prob.N)
+    err = lib().orc_f_all_tab(C.byref(h.s), _ptr(A, C.c_double), prob.tau, prob.f if f is None else f,
+                              _ptr(fp, C.c_double), _ptr(fk, C.c_double), nthreads)
+    if err:
+        raise ValueError({1: "row-zeroed nets are not periodic"}.get(err, "allocation failed"))
     return fk
 
 

@@ -332,6 +332,89 @@ int orc_f_all_meanid_tab(const orc_problem* p, const double* A, int tau, int f, 
   return 0;
 }
 
+/* O1+O2+O3 over ALL N rows for any f, for periodic kinds (lattice, column-deleted net, reduced MC):
+ * column j is tabulated from its plain definition at k = 0..M_j-1 (x_{k,j} depends only on k mod M_j,
+ * the tabulation SURVEY §8(c) allows), then the naive product Y[k,c] = sum_j x_{k,j} A[j,c]
+ * in increasing j (O2) on blocks of 32 rows x 64 columns (cache blocking only: every Y[k,c] is the
+ * same increasing-j sum as orc_product), and f_k = F(tau^-1 sum_c g(Y[k,c])) with the column sum
+ * carried across column blocks in increasing c (O3, as orc_f_row).  fk[k] for k = 0..N-1.
+ * Returns 1 for row-zeroed nets (not periodic), 2 on allocation failure. */
+int orc_f_all_tab(const orc_problem* p, const double* A, int tau, int f, const double* fp, double* fk,
+                  int nthreads) {
+  if (p->kind == 3) return 1;
+  const uint64_t N = ipow((uint64_t)p->b, p->m);
+  const int s = p->s;
+  uint64_t* M = (uint64_t*)malloc(sizeof(uint64_t) * s);
+  size_t* off = (size_t*)malloc(sizeof(size_t) * (s + 1));
+  if (!M || !off) { free(M); free(off); return 2; }
+  off[0] = 0;
+  for (int j = 0; j < s; ++j) {
+    int wj = p->w[j] < p->m ? p->w[j] : p->m;
+    M[j] = ipow((uint64_t)p->b, p->m - wj);
+    off[j + 1] = off[j] + M[j];
+  }
+  double* tab = (double*)malloc(sizeof(double) * off[s]);
+  if (!tab) { free(M); free(off); return 2; }
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int j = 0; j < s; ++j)
+    for (uint64_t r = 0; r < M[j]; ++r) tab[off[j] + r] = orc_point(p, r, j, NULL);
+  enum { RB = 32, CB = 64 };
+  int err = 0;
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * RB * s);
+    double* y = (double*)malloc(sizeof(double) * RB * CB);
+    double* acc = (double*)malloc(sizeof(double) * RB);
+    if (!x || !y || !acc) err = 2;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k0 = 0; k0 < (int64_t)N; k0 += RB) {
+      if (!x || !y || !acc) continue;
+      const int nr = (int64_t)N - k0 < RB ? (int)((int64_t)N - k0) : RB;
+      for (int i = 0; i < nr; ++i) {
+        for (int j = 0; j < s; ++j) x[i * s + j] = tab[off[j] + (uint64_t)(k0 + i) % M[j]];
+        acc[i] = 0.0;
+      }
+      for (int c0 = 0; c0 < tau; c0 += CB) {
+        const int nc = tau - c0 < CB ? tau - c0 : CB;
+        for (int i = 0; i < nr * CB; ++i) y[i] = 0.0;
+        for (int j = 0; j < s; ++j) {
+          const double* a = A + (size_t)j * tau + c0;
+          for (int i = 0; i < nr; ++i) {
+            const double xv = x[i * s + j];
+            double* yr = y + i * CB;
+#pragma omp simd
+            for (int c = 0; c < nc; ++c) yr[c] = yr[c] + xv * a[c];   /* independent c: no reordering */
+          }
+        }
+        for (int i = 0; i < nr; ++i)
+          for (int c = 0; c < nc; ++c) {
+            const double v = y[i * CB + c];
+            switch (f) {
+              case 1: acc[i] = acc[i] + exp(fp[0] * v); break;
+              case 2: acc[i] = acc[i] + v * v; break;
+              default: acc[i] = acc[i] + v; break;
+            }
+          }
+      }
+      for (int i = 0; i < nr; ++i) {
+        double r;
+        switch (f) {
+          case 0: r = exp(acc[i] / tau); break;
+          case 1: r = acc[i] / tau - fp[1]; r = r > 0.0 ? r : 0.0; break;
+          default: r = acc[i] / tau; break;
+        }
+        fk[k0 + i] = r;
+      }
+    }
+    free(x); free(y); free(acc);
+  }
+  free(tab); free(M); free(off);
+  return err;
+}
+
 /* Alg. 4, "fast reduced matrix product for digital nets", step by step, for the
  * unshifted, unmapped row-zeroed net (kind 3).  The input point set is the FULL digital net y_n of
  * Eq. def:digital (C^(j) without row zeroing); coordinate j uses the table

@@ -67,7 +67,7 @@ EXPORTS = ["rqmc_plan_create", "rqmc_plan_destroy", "rqmc_strerror", "rqmc_plan_
            "rqmc_plan_summary_get", "rqmc_plan_level", "rqmc_plan_global_row", "rqmc_plan_stats",
            "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_points",
            "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch",
-           "rqmc_plan_summary_batch"]
+           "rqmc_plan_summary_batch", "rqmc_plan_dispatch"]
 
 _lib = None
 
@@ -102,6 +102,7 @@ def lib():
         L.rqmc_plan_summary_batch.argtypes = [vp, C.c_int, C.c_int, C.POINTER(Summary)]
         L.rqmc_qn_batch.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), vp, i64,
                                     C.c_int, dp, vp, vp, C.c_size_t, vp]
+        L.rqmc_plan_dispatch.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
         L.rqmc_profile_read.argtypes = [vp, C.POINTER(C.c_int), dp, dp, dp, dp]
         _lib = L
     return _lib
@@ -169,6 +170,12 @@ class Plan:
             self._check(lib().rqmc_plan_level(self._h, i, C.byref(li)))
             out.append(li.as_dict())
         return out
+
+    def dispatch(self, f: int = F_MEAN, want_y: bool = False, R: int = 1) -> str:
+        """Name of the fused fine-level kernel template a run with these arguments launches (host only)."""
+        buf = C.create_string_buffer(96)
+        self._check(lib().rqmc_plan_dispatch(self._h, R, f, int(want_y), buf, len(buf)))
+        return buf.value.decode()
 
     def global_row(self, i: int) -> int:
         return lib().rqmc_plan_global_row(self._h, i)

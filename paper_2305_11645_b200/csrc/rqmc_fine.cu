@@ -15,6 +15,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -501,22 +502,52 @@ static bool bottom_matches(const FineArgs& a) {
   return true;
 }
 
+// bottom block of the general kernel: 0 BotNone, 1 BotB2, 2 BotB2s, 3 BotB3 (host; the dispatch decision)
+static int bottom_select(const FineArgs& a) {
+  if (a.NF >= 3 && bottom_matches<BotB2>(a)) return 1;
+  if (a.NF >= 2 && bottom_matches<BotB2s>(a)) return 2;
+  if (a.NF >= 2 && bottom_matches<BotB3>(a)) return 3;
+  return 0;
+}
+
 template <int NF>
 static cudaError_t launch_fine_n(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st) {
+  const int bs = bottom_select(a);
   if constexpr (NF >= 3)
-    if (bottom_matches<BotB2>(a)) return launch_fine_t<NF, BotB2>(a, nb, nrep, st);
+    if (bs == 1) return launch_fine_t<NF, BotB2>(a, nb, nrep, st);
   if constexpr (NF >= 2) {
-    if (bottom_matches<BotB2s>(a)) return launch_fine_t<NF, BotB2s>(a, nb, nrep, st);
-    if (bottom_matches<BotB3>(a)) return launch_fine_t<NF, BotB3>(a, nb, nrep, st);
+    if (bs == 2) return launch_fine_t<NF, BotB2s>(a, nb, nrep, st);
+    if (bs == 3) return launch_fine_t<NF, BotB3>(a, nb, nrep, st);
   }
   return launch_fine_t<NF, BotNone>(a, nb, nrep, st);
 }
 
 cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts);
+int tree_select(const FineArgs& a);
+int64_t tree_split(const FineArgs& a, int64_t* nbt);
+
+static bool no_tree() { const char* e = std::getenv("RQMC_NO_TREE"); return e != nullptr && *e && *e != '0'; }
+
+// The kernel template launch_fine picks for these arguments, e.g. "k_fine_tree<6,2,g=1,Y=0>" or
+// "k_fine<4,BotB2>" (g: 0 none, 1 identity, 2 exp, 3 square; tests assert which branch they reach).
+int describe_fine(const FineArgs& a, char* buf, size_t n) {
+  const int g = a.fk < 0 ? 0 : (a.fk == 1 ? 2 : (a.fk == 2 ? 3 : 1));
+  const int ts = no_tree() ? 0 : tree_select(a);
+  if (ts) {
+    int64_t nbt = 0;
+    const int64_t first = tree_split(a, &nbt);
+    if (first < nbt)   // tail split active (b = 3 with f, a device present): bundles [first, nbt) split
+      return snprintf(buf, n, "k_fine_tree<%d,%d,g=%d,Y=%d>split=%lld/%lld", ts / 10, ts % 10, g,
+                      a.Y != nullptr ? 1 : 0, (long long)first, (long long)nbt);
+    return snprintf(buf, n, "k_fine_tree<%d,%d,g=%d,Y=%d>", ts / 10, ts % 10, g, a.Y != nullptr ? 1 : 0);
+  }
+  static const char* bots[4] = {"BotNone", "BotB2", "BotB2s", "BotB3"};
+  return snprintf(buf, n, "k_fine<%d,%s>", a.NF, bots[a.NF == 0 ? 0 : bottom_select(a)]);
+}
 
 cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
   *nparts = nb;
-  if (std::getenv("RQMC_NO_TREE") == nullptr) {
+  if (!no_tree()) {
     const cudaError_t e = launch_tree(a, nb, nrep, st, nparts);
     if (e != cudaErrorNotSupported) return e;
   }

@@ -90,6 +90,8 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st);
 // nparts: partial sums written per replica (the tree kernel's bundles may be smaller than kBundle;
 // the workspace holds 4 nbundles partials per replica)
 cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, int nrep, cudaStream_t st, int64_t* nparts);
+// host only: the fine-kernel template launch_fine would pick (for tests / rqmc_plan_dispatch)
+int describe_fine(const FineArgs& a, char* buf, size_t n);
 cudaError_t launch_reduce(const double* partial, int64_t n, int64_t stride, int nrep, double* out, cudaStream_t st);
 
 }  // namespace rqmc

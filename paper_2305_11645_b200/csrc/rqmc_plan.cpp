@@ -523,6 +523,42 @@ rqmc_status check_cuda(rqmc_plan_s* p, cudaError_t e, const char* what) {
   return fail(p, RQMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Arguments of the fused fine kernel for layout `lay` on workspace w (X: X^red base of the slice).
+FineArgs fine_args(const rqmc_plan_s* p, const Layout& lay, char* w, double* X, const double* dA, int64_t lda,
+                   double* dY, int64_t ldy, int fk, const double* fparam, int64_t rep_d) {
+  FineArgs fa{};
+  const Level& R = lay.lv[lay.ckpt];
+  fa.root = reinterpret_cast<const double*>(w + lay.off_r[R.rbuf]); fa.ldroot = lay.ldr; fa.Mroot = R.Ml;
+  fa.NF = lay.nfine;
+  for (int i = 0; i < lay.nfine; ++i) {
+    const Level& L = lay.lv[lay.ckpt + 1 + i];
+    FineLevel& F = fa.lv[i];
+    F.X = X + L.xoff; F.ldx = L.ldx; F.K = L.s_w; F.j_lo = L.j_lo;
+    F.runs = (int)(L.Ml / R.Ml);
+    F.fan = i == 0 ? F.runs : F.runs / fa.lv[i - 1].runs;
+    F.xs_off = lay.fine_xs_off[i]; F.as_off = lay.fine_as_off[i];
+  }
+  fa.A = dA; fa.lda = lda; fa.tau = p->tau;
+  fa.a_vec = ((uintptr_t)dA % 16 == 0) && (lda % 2 == 0) && (p->tau % 2 == 0);
+  fa.Y = dY; fa.ldy = ldy;
+  fa.y_vec = ((uintptr_t)dY % 16 == 0) && (ldy % 2 == 0);
+  fa.fk = fk;
+  fa.fp0 = fparam ? fparam[0] : 0.0;
+  fa.fp1 = fparam ? fparam[1] : 0.0;
+  fa.partial = reinterpret_cast<double*>(w + lay.off_part);
+  fa.leafruns = lay.leafruns;
+  fa.as_stride = lay.fine_as_stride;
+  fa.root_off = 2 * lay.fine_as_stride;
+  fa.acc_off = lay.fine_acc_off;
+  fa.smem_bytes = lay.fine_smem;
+  fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
+  if (lay.split_cap) {
+    fa.rscr = reinterpret_cast<double*>(w + lay.off_split); fa.rscr_cap = lay.split_cap;
+    fa.rcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); fa.ncnt = kSplitSlots;
+  }
+  return fa;
+}
+
 // One pass of the hot path for nrep replicas (batched randomisation) whose workspace slices of
 // rep_bytes each start at `base`: replica r uses shift[r*srep + j] / dshift[...] / seeds[r].
 // nrep = 1 with the plan's own tables is the plain run.
@@ -584,36 +620,7 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   mark(2);
 
   // a3+a4+a5 fine levels fused with f / Y store
-  FineArgs fa{};
-  const Level& R = lay.lv[lay.ckpt];
-  fa.root = reinterpret_cast<const double*>(w + lay.off_r[R.rbuf]); fa.ldroot = lay.ldr; fa.Mroot = R.Ml;
-  fa.NF = lay.nfine;
-  for (int i = 0; i < lay.nfine; ++i) {
-    const Level& L = lay.lv[lay.ckpt + 1 + i];
-    FineLevel& F = fa.lv[i];
-    F.X = g.X + L.xoff; F.ldx = L.ldx; F.K = L.s_w; F.j_lo = L.j_lo;
-    F.runs = (int)(L.Ml / R.Ml);
-    F.fan = i == 0 ? F.runs : F.runs / fa.lv[i - 1].runs;
-    F.xs_off = lay.fine_xs_off[i]; F.as_off = lay.fine_as_off[i];
-  }
-  fa.A = dA; fa.lda = lda; fa.tau = p->tau;
-  fa.a_vec = ((uintptr_t)dA % 16 == 0) && (lda % 2 == 0) && (p->tau % 2 == 0);
-  fa.Y = dY; fa.ldy = ldy;
-  fa.y_vec = ((uintptr_t)dY % 16 == 0) && (ldy % 2 == 0);
-  fa.fk = want_f ? (int)f : -1;
-  fa.fp0 = fparam ? fparam[0] : 0.0;
-  fa.fp1 = fparam ? fparam[1] : 0.0;
-  fa.partial = reinterpret_cast<double*>(w + lay.off_part);
-  fa.leafruns = lay.leafruns;
-  fa.as_stride = lay.fine_as_stride;
-  fa.root_off = 2 * lay.fine_as_stride;
-  fa.acc_off = lay.fine_acc_off;
-  fa.smem_bytes = lay.fine_smem;
-  fa.xrep = rep_d; fa.rootrep = rep_d; fa.partrep = rep_d;
-  if (lay.split_cap) {
-    fa.rscr = reinterpret_cast<double*>(w + lay.off_split); fa.rscr_cap = lay.split_cap;
-    fa.rcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); fa.ncnt = kSplitSlots;
-  }
+  const FineArgs fa = fine_args(p, lay, w, g.X, dA, lda, dY, ldy, want_f ? (int)f : -1, fparam, rep_d);
   int64_t nparts = 0;
   if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st, &nparts), "k_fine")) return s;
   mark(3);
@@ -779,22 +786,29 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
   }
   // layout for the replicas that run together; a smaller workspace means smaller chunks, which
   // may in turn want a finer checkpoint (re-evaluated until stable)
-  const Layout* lay = &layout_for(p, R, f);
-  int64_t chunk = R;
-  for (int it = 0; it < 4; ++it) {
-    chunk = R;
-    while (chunk > 0 && batch_bytes(p, *lay, chunk) > wbytes) --chunk;
-    if (chunk == 0) break;
+  // (chunks <= 65535 replicas: the replica count is a grid dimension of every kernel)
+  const int64_t cmax = std::min<int64_t>(R, 65535);
+  auto fit = [&](const Layout& L) {
+    int64_t n = cmax;
+    while (n > 0 && batch_bytes(p, L, n) > wbytes) --n;
+    return n;
+  };
+  const Layout* lay = &layout_for(p, cmax, f);
+  int64_t chunk = fit(*lay);
+  for (int it = 0; it < 8 && chunk > 0; ++it) {
     const Layout* l2 = &layout_for(p, chunk, f);
     if (l2 == lay) break;
     lay = l2;
+    chunk = fit(*lay);   // the chunk is always sized for the layout it runs with
   }
   if (chunk == 0) {
     lay = &p->L1;
-    chunk = wbytes >= batch_bytes(p, *lay, 1) ? 1 : 0;
+    chunk = fit(*lay) > 0 ? 1 : 0;
   }
   if (chunk == 0) return fail(p, RQMC_EINVAL, "workspace too small for one replica: need " +
                                                   std::to_string(batch_bytes(p, p->L1, 1)));
+  if (batch_bytes(p, *lay, chunk) > wbytes)
+    return fail(p, RQMC_EINVAL, "internal: batch chunk exceeds the workspace");
   if (rqmc_status s = upload(p)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(dwork);
@@ -812,6 +826,21 @@ rqmc_status rqmc_qn_batch(rqmc_plan_t p, int R, const double* hshifts, const uin
                                  d_fsum + r0, st))
       return s;
   }
+  return RQMC_OK;
+}
+
+rqmc_status rqmc_plan_dispatch(rqmc_plan_t p, int R, int f, int want_y, char* buf, size_t len) {
+  if (!p || !buf || len == 0 || R < 1) return RQMC_EINVAL;
+  const Layout& lay = R == 1 ? p->L1 : layout_for(p, R, f);
+  // placeholder addresses: 256-byte aligned, never dereferenced (only alignment and NULL-ness matter)
+  char* w = reinterpret_cast<char*>(uintptr_t(1) << 20);
+  double* X = reinterpret_cast<double*>(w + lay.off_x);
+  const double* dA = reinterpret_cast<const double*>(w);
+  double* dY = want_y ? reinterpret_cast<double*>(w) : nullptr;
+  const int fk = f == RQMC_F_NONE ? -1 : f;
+  const FineArgs fa = fine_args(p, lay, w, X, dA, p->tau + (p->tau & 1), dY, p->tau + (p->tau & 1), fk, nullptr,
+                                (int64_t)(lay.off_fsum / sizeof(double)));
+  describe_fine(fa, buf, len);
   return RQMC_OK;
 }
 

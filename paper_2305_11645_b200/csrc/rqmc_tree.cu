@@ -213,12 +213,13 @@ __device__ __constant__ static const double kExp2Tab64[64] = {
     1.978456026387951
 };
 
-// exp(x) for the elementwise g = exp(p0 y) of C2 (|x| <= 700, clamped): x = (k/64) ln 2 + r with
+// exp(x) for the elementwise g = exp(p0 y) of C2 (|x| <= 700; NaN, +-inf and |x| > 700 go to libdevice
+// exp, so overflow / underflow / NaN propagate exactly as in the general kernel): x = (k/64) ln 2 + r with
 // |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
 // (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
 // exponent field.  11 fp64 instructions + 1 LDS vs 16 fp64 + branch for exp(); <= ~2.5 ulp.
 __device__ __forceinline__ double exp_t(double x, const double* etab) {
-  x = fmin(fmax(x, -700.0), 700.0);
+  if (__builtin_expect(!(fabs(x) <= 700.0), 0)) return exp(x);
   const double kd = rint(x * 92.33248261689366);                 // 64 / ln 2
   double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
   r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
@@ -739,6 +740,40 @@ constexpr int tree_passes() {
   return (RQMC_TREE_WIDE && Tree<NF, B, tree_nfr<NF, B>(), RQMC_TREE_BUNDLE, 2>::SMEM <= 100 * 1024) ? 2 : 1;
 }
 
+// Tail split (b = 3 trees with f): when the fine grid's last wave would be at most half full, its
+// bundles run as two CTAs over half the column tiles each.  Returns the first split bundle (nbt when
+// nothing splits).  The decision depends only on the bundle count and on the kernel's occupancy on
+// kSplitSMs = 148 SMs (a constant, not the device's SM count), so a given binary splits -- and sums --
+// identically on every device it runs on, and a replica of a batch sums like a single run.
+constexpr int kSplitSMs = 148;
+template <int NF, int B, int G, bool STY>
+static int64_t tree_split_first(const FineArgs& a, int64_t nbt) {
+  constexpr int NFR = tree_nfr<NF, B>(), BUN = tree_bundle<NF, B>(), NH = tree_passes<NF, B>();
+  using T = Tree<NF, B, NFR, BUN, NH>;
+  if constexpr (B == 3 && G > 0 && T::SMEM <= 227 * 1024) {
+    static const bool no_split = [] { const char* v = std::getenv("RQMC_NO_SPLIT"); return v && *v && *v != '0'; }();
+    const int ntiles = (a.tau + T::CW - 1) / T::CW;
+    if (no_split || !a.rscr || ntiles < 2) return nbt;
+    static const int64_t slots = [] {
+      int occ = 0;
+      if (set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::SMEM) != cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::THREADS,
+                                                        T::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 0;   // no device (host-only inspection): no split
+      }
+      return (int64_t)occ * kSplitSMs;
+    }();
+    // RQMC_FORCE_SPLIT=1 (tests): split every bundle, so small problems exercise the combine path
+    const char* fv = std::getenv("RQMC_FORCE_SPLIT");
+    const bool force = fv && *fv && *fv != '0';
+    const int64_t tail = force ? nbt : (slots > 0 && nbt >= slots) ? nbt % slots : 0;
+    if (tail > 0 && (force || 2 * tail <= slots) && tail <= a.ncnt && tail * 2 * (int64_t)T::LEAVES * BUN <= a.rscr_cap)
+      return nbt - tail;
+  }
+  return nbt;
+}
+
 template <int NF, int B, int G, bool STY>
 static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
   constexpr int NFR = tree_nfr<NF, B>(), BUN = tree_bundle<NF, B>(), NH = tree_passes<NF, B>();
@@ -751,34 +786,9 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
   *nparts = nbt;
-  // tail split (b = 3): when the last wave would be at most half full, its bundles run as two CTAs over
-  // half the column tiles each (decided from nbt alone, so a replica of a batch sums like a single run)
   FineArgs b = a;
-  b.nfull = nbt;
-  b.nsplit = 1;
-  if constexpr (B == 3 && G > 0) {
-    static const bool no_split = [] { const char* v = std::getenv("RQMC_NO_SPLIT"); return v && *v && *v != '0'; }();
-    const int ntiles = (a.tau + T::CW - 1) / T::CW;
-    if (!no_split && a.rscr && ntiles >= 2) {
-      static const int64_t slots = [] {
-        int occ = 0, dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::THREADS,
-                                                      T::SMEM);
-        return (int64_t)occ * nsm;
-      }();
-      // RQMC_FORCE_SPLIT=1 (tests): split every bundle, so small problems exercise the combine path
-      const char* fv = std::getenv("RQMC_FORCE_SPLIT");
-      const bool force = fv && *fv && *fv != '0';
-      const int64_t tail = force ? nbt : (slots > 0 && nbt >= slots) ? nbt % slots : 0;
-      if (tail > 0 && (force || 2 * tail <= slots) && tail <= a.ncnt &&
-          tail * 2 * (int64_t)T::LEAVES * BUN <= a.rscr_cap) {
-        b.nfull = nbt - tail;
-        b.nsplit = 2;
-      }
-    }
-  }
+  b.nfull = tree_split_first<NF, B, G, STY>(a, nbt);
+  b.nsplit = b.nfull < nbt ? 2 : 1;
   const int64_t grid = b.nfull + (nbt - b.nfull) * b.nsplit;
   return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)grid, (unsigned)nrep), dim3(T::THREADS),
                   (size_t)T::SMEM, st, false, b);
@@ -807,18 +817,54 @@ static cudaError_t launch_tree_g(const FineArgs& a, int64_t nb, int nrep, cudaSt
   }
 }
 
+// Which compile-time tree the fine level table matches: 10 NF + B, or 0 (none / nothing to consume).
+// (No 7-level tree: the planner's shared-memory bound never fuses 7 levels of the log_2 shape.)
+// Host only; the single source of the dispatch decision (launch_tree and describe_fine).
+int tree_select(const FineArgs& a) {
+  if (a.Y == nullptr && a.fk < 0) return 0;
+  if (tree_matches<6, 2>(a)) return 62;
+  if (tree_matches<5, 2>(a)) return 52;
+  if (tree_matches<4, 2>(a)) return 42;
+  if (tree_matches<3, 2>(a)) return 32;
+  if (tree_matches<2, 2>(a)) return 22;
+  if (tree_matches<3, 3>(a)) return 33;
+  if (tree_matches<2, 3>(a)) return 23;
+  return 0;
+}
+
+// First tail-split bundle of the tree launch (and the bundle count), for describe_fine; -1: no tree.
+template <int NF, int B>
+static int64_t tree_split_g(const FineArgs& a, int64_t* nbt) {
+  constexpr int BUN = tree_bundle<NF, B>();
+  *nbt = (a.Mroot + BUN - 1) / BUN;
+  const bool sty = a.Y != nullptr;
+  switch (a.fk) {
+    case -1: return *nbt;
+    case 1: return sty ? tree_split_first<NF, B, 2, true>(a, *nbt) : tree_split_first<NF, B, 2, false>(a, *nbt);
+    case 2: return sty ? tree_split_first<NF, B, 3, true>(a, *nbt) : tree_split_first<NF, B, 3, false>(a, *nbt);
+    default: return sty ? tree_split_first<NF, B, 1, true>(a, *nbt) : tree_split_first<NF, B, 1, false>(a, *nbt);
+  }
+}
+int64_t tree_split(const FineArgs& a, int64_t* nbt) {
+  switch (tree_select(a)) {
+    case 33: return tree_split_g<3, 3>(a, nbt);
+    case 23: return tree_split_g<2, 3>(a, nbt);
+    default: *nbt = 0; return 0;   // b = 2 trees never split
+  }
+}
+
 // returns cudaErrorNotSupported when no compile-time tree matches
 cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* np) {
-  if (a.Y == nullptr && a.fk < 0) return cudaErrorNotSupported;
-  if (tree_matches<6, 2>(a)) return launch_tree_g<6, 2>(a, nb, nrep, st, np);
-  if (tree_matches<5, 2>(a)) return launch_tree_g<5, 2>(a, nb, nrep, st, np);
-  if (tree_matches<4, 2>(a)) return launch_tree_g<4, 2>(a, nb, nrep, st, np);
-  if (tree_matches<3, 2>(a)) return launch_tree_g<3, 2>(a, nb, nrep, st, np);
-  if (tree_matches<2, 2>(a)) return launch_tree_g<2, 2>(a, nb, nrep, st, np);
-  if (tree_matches<7, 2>(a)) return launch_tree_g<7, 2>(a, nb, nrep, st, np);
-  if (tree_matches<3, 3>(a)) return launch_tree_g<3, 3>(a, nb, nrep, st, np);
-  if (tree_matches<2, 3>(a)) return launch_tree_g<2, 3>(a, nb, nrep, st, np);
-  return cudaErrorNotSupported;
+  switch (tree_select(a)) {
+    case 62: return launch_tree_g<6, 2>(a, nb, nrep, st, np);
+    case 52: return launch_tree_g<5, 2>(a, nb, nrep, st, np);
+    case 42: return launch_tree_g<4, 2>(a, nb, nrep, st, np);
+    case 32: return launch_tree_g<3, 2>(a, nb, nrep, st, np);
+    case 22: return launch_tree_g<2, 2>(a, nb, nrep, st, np);
+    case 33: return launch_tree_g<3, 3>(a, nb, nrep, st, np);
+    case 23: return launch_tree_g<2, 3>(a, nb, nrep, st, np);
+    default: return cudaErrorNotSupported;
+  }
 }
 
 }  // namespace rqmc

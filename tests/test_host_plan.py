@@ -244,3 +244,50 @@ def test_run_call_validation(rq):
     ok = (C.c_double * 8)(*([0.5] * 8))
     assert L.rqmc_qn_batch(q._h, 2, ok, None, None, fake, 3, 0, fp, fs, fake, 1 << 30, st) == 1   # EINVAL
     assert L.rqmc_points(p._h, 99, 0, 1, None, None, st) == 1                           # EINVAL (level)
+
+
+def test_fine_dispatch_table(rq, monkeypatch):
+    """Host-only: every fused-fine parity case of tests/test_gpu_fine_paths.py plans the kernel template
+    and fused depth it is meant to cover (rqmc_plan_dispatch; DESIGN.md §7 "Dispatch coverage")."""
+    from test_gpu_fine_paths import CASES, RANK_CASES, make_prob
+    for cid, (b, m, s, tau, wmode, kind, mapping, ck, nt, tmpl, nf) in CASES.items():
+        monkeypatch.setenv("RQMC_CKPT_W", ck)
+        monkeypatch.setenv("RQMC_NO_TREE", "1" if nt else "0")
+        prob = make_prob(500 + sum(map(ord, cid)), b, m, s, tau, wmode, kind=kind, mapping=mapping)
+        pl = rq.Plan.from_problem(prob)
+        assert pl.summary()["n_fine"] == nf, cid
+        assert pl.dispatch(W.F_EXP_MEAN, want_y=False).startswith(tmpl), (cid, pl.dispatch(W.F_EXP_MEAN))
+    for cid, G, ck, tmpl, nf in RANK_CASES:
+        b, m, s, tau, wmode, kind, mapping, _, nt, _, _ = CASES[cid]
+        monkeypatch.setenv("RQMC_CKPT_W", ck)
+        monkeypatch.setenv("RQMC_NO_TREE", "1" if nt else "0")
+        prob = make_prob(700 + sum(map(ord, cid)) + G, b, m, s, tau, wmode, kind=kind, mapping=mapping)
+        for g in range(G):
+            pl = rq.Plan.from_problem(prob, rank=g, world=G)
+            assert pl.summary()["n_fine"] == nf and pl.dispatch(W.F_MEAN).startswith(tmpl), (cid, G, g)
+
+
+def test_batch_chunk_fits_workspace(rq):
+    """a tight workspace makes rqmc_qn_batch re-plan its chunk / layout; whatever it picks
+    must fit the caller's bytes (the call validates before launching: on a host without a device it
+    gets as far as the upload and fails with ECUDA, never EINVAL for a workspace that holds one
+    replica)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host-only check (passes placeholder device pointers)")
+    prob = W.make_random(5, 2, 14, 100, 40, shifted=True, mapping=W.MAP_INVNORM)
+    pl = rq.Plan.from_problem(prob)
+    one, many = pl.workspace_size_batch(1), pl.workspace_size_batch(64)
+    assert many > one
+    lib = rq.lib()
+    sh = np.random.default_rng(0).random((64, prob.s))
+    out = (C.c_double * 64)()
+    for wb in (one, (one + many) // 3, many - 8, many):
+        st = lib.rqmc_qn_batch(pl._h, 64, sh.ctypes.data_as(C.POINTER(C.c_double)), None, None,
+                               C.c_void_p(1 << 20), prob.tau, W.F_EXP_MEAN, None,
+                               C.cast(out, C.c_void_p), C.c_void_p(1 << 30), wb, None)
+        assert st in (0, 9), (wb, st)              # RQMC_OK on a GPU would need real buffers; ECUDA here
+    st = lib.rqmc_qn_batch(pl._h, 64, sh.ctypes.data_as(C.POINTER(C.c_double)), None, None,
+                           C.c_void_p(1 << 20), prob.tau, W.F_EXP_MEAN, None, C.cast(out, C.c_void_p),
+                           C.c_void_p(1 << 30), one - 8, None)
+    assert st == 1                                 # EINVAL: below one replica

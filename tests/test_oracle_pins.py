@@ -233,6 +233,35 @@ def test_zero_rule():
     assert X[8, 0] == 0.0 and X[4, 1] == 0.0       # u = 1/2 -> 0
 
 
+def test_zero_rule_shifted():
+    """Reading C-5, shifted branch: a shifted coordinate that wraps to exactly u = 0 is mapped as
+    u = 2^-53.  G1s (tests/golden/g1s_lattice_shift.txt) has x_{k,3} = {k/2 + 1/2} = 0 for every
+    odd k, so with Phi^-1 those entries are Phi^-1(2^-53) -- pinned against scipy's ndtri (an
+    independent library routine), like every other G1s entry against ndtri of its golden value."""
+    from scipy.special import ndtri
+    p = lattice(2, 3, [0, 1, 2], [3, 1, 1], [1 / 16, 3 / 8, 1 / 2], mapping=W.MAP_INVNORM)
+    X, T = oracle.points(p)
+    unit = oracle.points(lattice(2, 3, [0, 1, 2], [3, 1, 1], [1 / 16, 3 / 8, 1 / 2]))[0]
+    for k in range(8):
+        for j in range(3):
+            u = unit[k, j]
+            ref = ndtri(2.0 ** -53) if u == 0.0 else ndtri(u)
+            assert abs(X[k, j] - ref) <= 2e-15 * max(1.0, abs(ref)), (k, j)
+    assert all(unit[k, 2] == 0.0 for k in (1, 3, 5, 7))          # the wrap happens (golden table)
+    assert abs(X[1, 2] - (-8.209536151601387)) <= 2e-14            # Phi^-1(2^-53) (scipy ndtri)
+
+
+def test_f_all_tab_equals_rowwise():
+    """The full-N oracle with column tabulation and cache blocking (orc_f_all_tab) is the plain
+    O1+O2+O3 path reorganised without changing any per-entry operation order: bit-identical to
+    f_rows on every kind, map, shift and f (including ragged row / column blocks)."""
+    for kind, b, m in ((W.KIND_LATTICE, 2, 7), (W.KIND_LATTICE, 3, 5), (W.KIND_NET, 2, 7), (W.KIND_MC, 2, 6)):
+        for f in (W.F_EXP_MEAN, W.F_CALL_MEAN_EXP, W.F_MEAN_SQ, W.F_MEAN):
+            prob = W.make_random(90 + f, b, m, 71, 131, kind=kind, shifted=kind != W.KIND_MC,
+                                 mapping=W.MAP_INVNORM if f % 2 else W.MAP_UNIT, wmode="rand", f=f)
+            assert np.array_equal(oracle.f_all_tab(prob), oracle.f_rows(prob, np.arange(prob.N)))
+
+
 # ---------------------------------------------------------------- product (O2) and Q_N (O3)
 
 def _frac_points(b, m, w, z, shift_fr=None):
