@@ -560,7 +560,6 @@ cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st
     case 5: return launch_fine_n<5>(a, nb, nrep, st);
     case 6: return launch_fine_n<6>(a, nb, nrep, st);
     case 7: return launch_fine_n<7>(a, nb, nrep, st);
-    case 8: return launch_fine_n<8>(a, nb, nrep, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -9,7 +9,7 @@
 namespace rqmc {
 
 constexpr int kMaxLevels = 64;
-constexpr int kMaxFine = 8;       // fused fine levels (compile-time DFS depth)
+constexpr int kMaxFine = 7;       // fused fine levels (compile-time DFS depth; 8 never fits the smem bound)
 constexpr int kBundle = 32;       // residues of the checkpoint level per fine CTA
 constexpr int kSplitSlots = 512;  // max tail bundles split over two CTAs (FineArgs::rscr)
 constexpr int kFineBN = 32;       // column tile of the fine kernel
