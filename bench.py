@@ -8,7 +8,9 @@ local f-sums.  value = N*tau / (max over ranks of the device time per step) -- t
 
 Default workload: BASELINE configs[4] = C5 (b=2, m=24, s=4096, tau=2048, shift, Phi^-1,
 f = exp(mean)), the config the north-star target is stated on; it fits one GPU (Y never stored).
-Multi-GPU (torchrun): rank g owns the points k = g (mod G) of the SAME problem (strong scaling).
+Multi-GPU (torchrun): rank g owns residue classes of the point index of the SAME problem (k = g mod G
+when G is a power of b; contiguous groups of b^gamma classes otherwise; strong scaling).
+`--dist-backend gloo` is a dry run of that path with the ranks sharing the visible GPU(s).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
 """
@@ -164,6 +166,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: dry run of the N > 1 path with all ranks sharing the visible GPU(s) "
+                         "(barrier, all_reduce, max-over-ranks timing; not a scaling measurement)")
     ap.add_argument("--replicas", type=int, default=1,
                     help="R > 1: batched randomisation (rqmc_qn_batch) of R shifts / seeds per step")
     args = ap.parse_args()
@@ -178,13 +183,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()     # dry run: ranks may share one GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert world == args.gpus or world == 1, "launch with torchrun --nproc-per-node N for --gpus N"
 
     plan = rq.Plan.from_problem(prob, rank=rank, world=world)
     summ = plan.summary()
+    part = plan.partition()
     A = torch.from_numpy(prob.A).cuda()
     fsum = torch.zeros(1, dtype=torch.float64, device="cuda")
     ws = plan.workspace()
@@ -193,7 +204,7 @@ def main():
 
     Y = None
     if prob.store_y and args.replicas == 1:   # configs whose output is the full XA (C1, C4): Y written every step
-        Y = torch.empty((prob.N // world, prob.tau), dtype=torch.float64, device="cuda")
+        Y = torch.empty((summ["N_local"], prob.tau), dtype=torch.float64, device="cuda")
     R = args.replicas
     rkw = {}
     if R > 1:   # R independent randomisations of the same plan
@@ -313,7 +324,7 @@ def main():
     algo = fine_flops if dominant == "k_fine" else coarse_flops
     if dominant == "k_fine" and Y is not None:
         # XA stored: the fused fine kernel streams Y (8 N tau bytes) to HBM -- the bound
-        algo = 8.0 * (prob.N // world) * prob.tau
+        algo = 8.0 * summ["N_local"] * prob.tau
         ach, bound, unit = algo / (fine_ms * 1e-3) / 1e9, "hbm", "GB/s"
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -333,7 +344,7 @@ def main():
                 if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0)
     t_step = ms_max / args.steps * 1e-3
     f_step = total_flops          # rqmc_plan_stats counts this rank's local rows already
-    b_step = 8.0 * prob.s * prob.tau + (8.0 * (prob.N // world) * prob.tau if Y is not None else 0.0)
+    b_step = 8.0 * prob.s * prob.tau + (8.0 * summ["N_local"] * prob.tau if Y is not None else 0.0)
     t_roof = max(f_step / p64, b_step / bw)
     step_roof = {"flops_per_step": f_step, "bytes_per_step": b_step,
                  "bound": "fp64" if f_step / p64 >= b_step / bw else "hbm",
@@ -356,7 +367,9 @@ def main():
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": describe(prob), "N": prob.N, "s": prob.s, "tau": prob.tau,
-                   "parallelism": f"residue classes k mod {world}" if world > 1 else "single GPU",
+                   "parallelism": (f"residue classes: {part['classes']} classes k mod {part['classes']}, "
+                                   f"contiguous groups per rank, {world} ranks ({args.dist_backend})")
+                                  if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write, outside the step events)",
                    "checkpoint_w": levels[ck]["w"], "fused_fine_levels": summ["n_fine"],
                    "replicas": R},

@@ -23,13 +23,20 @@
  *    first run call, thread-safely): concurrent runs on distinct streams with distinct outputs and
  *    workspaces are safe.
  *  - Layouts: A row-major s x tau, row j = a_j, leading dimension lda >= tau (elements).
- *    Y row-major (N/world) x tau, ldy >= tau; local row i is global point k = rank + world * i
- *    (residue-class partition, multi-GPU; world = 1 gives Y = XA).
+ *    Y row-major N_local x tau, ldy >= tau.  Multi-GPU residue-class partition:
+ *    the points are split into ncls classes k mod ncls and rank g owns the contiguous classes
+ *    c0 .. c0+nc-1 (rqmc_plan_partition); local row i is global point
+ *        k = c0 + (i mod nc) + ncls * (i div nc),      N_local = nc * N / ncls.
+ *    world a power of b dividing N: ncls = world, c0 = rank, nc = 1 (k = rank + world * i), so every
+ *    level with M_w >= world splits exactly.  Any other world (b = 3 on 2/4/8 GPUs, ...): ncls = b^gamma,
+ *    the smallest power >= 32 world (gamma <= m), in groups of floor/ceil(ncls/world) classes (work
+ *    imbalance <= 3 %).  Levels with fewer than ncls rows keep nc replicated rows per rank.
+ *    world = 1 gives Y = XA.
  *  - Point kinds: RQMC_LATTICE, RQMC_DIGITAL_NET (b = 2), RQMC_REDUCED_MC and
  *    RQMC_DIGITAL_NET_ROWS (row-zeroed nets, Alg. 4) (see rqmc_kind).
  *  - Precision: fp64 throughout.  Point indices/digits are exact integers; lattice values are
  *    u = t/M (IEEE divide), shift u = u + Delta, if u >= 1 then u - 1 (no FMA contraction).
- *  - Limits: N = b^m <= 2^32; m <= 53 for nets; world must be a power of b dividing N.
+ *  - Limits: N = b^m <= 2^32; m <= 32 for nets; 1 <= world <= N.
  */
 #ifndef RQMC_H
 #define RQMC_H
@@ -105,7 +112,7 @@ typedef struct {
   const double* shift;      /* lattice random shift Delta_j in [0,1), or NULL        */
   const uint64_t* dshift;   /* net digital shift sigma_j < 2^53: x = ((W << (53-m)) ^ sigma) 2^-53 */
   rqmc_map map;             /* RQMC_MAP_INVNORM: x = Phi^-1(u), u = 0 remapped (reading C-5) */
-  int rank, world;          /* residue-class partition k = rank (mod world); (0,1) = whole   */
+  int rank, world;          /* residue-class partition (see Layouts); (0,1) = whole problem  */
   uint64_t seed;            /* RQMC_REDUCED_MC: generator seed (z, C, shift, dshift unused)  */
 } rqmc_plan_desc;
 
@@ -114,7 +121,7 @@ typedef struct {
   int w;            /* level index min(w_j, m) (m = constant level of shifted w_j >= m)        */
   int j_lo, s_w;    /* 0-based coordinates j_lo .. j_lo+s_w-1 (tau_w = s_w)             */
   int64_t M;        /* global distinct rows b^{m-w}                                            */
-  int64_t M_local;  /* rows on this rank: max(M / world, 1)                                    */
+  int64_t M_local;  /* rows on this rank: nc M / ncls if M >= ncls, else nc (replicated)       */
   int parent;       /* index of the next coarser non-empty level, -1 for the top               */
   int coarse;       /* 1: materialised per-level GEMM pass; 0: fused into the fine kernel      */
 } rqmc_level_info;
@@ -124,7 +131,7 @@ typedef struct {
   int checkpoint;           /* index of the last coarse level (root of the fine kernel)      */
   int n_fine;               /* fused fine levels below the checkpoint                        */
   int64_t n_bundles;        /* fine-kernel CTAs (bundles of residues of the checkpoint)      */
-  int64_t N_local;          /* N / world                                                     */
+  int64_t N_local;          /* nc N / ncls (= N / world when world is a power of b)          */
   int s_star;               /* s* = max{j : w_j < m}                                 */
 } rqmc_plan_summary;
 
@@ -135,8 +142,11 @@ const char* rqmc_plan_last_error(rqmc_plan_t p);
 
 rqmc_status rqmc_plan_summary_get(rqmc_plan_t p, rqmc_plan_summary* out);
 rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* out);
-/* Global point index k of local row i (k = rank + world*i). */
+/* Global point index k of local row i (k = c0 + (i mod nc) + ncls (i div nc)); -1 if out of range. */
 int64_t     rqmc_plan_global_row(rqmc_plan_t p, int64_t i);
+/* Residue-class partition of this rank (see Layouts): ncls classes k mod ncls, this rank owns classes
+ * first .. first+count-1.  Any output may be NULL. */
+rqmc_status rqmc_plan_partition(rqmc_plan_t p, int64_t* classes, int64_t* first, int64_t* count);
 /* Counter law: local rows, algorithmic MACs tau * sum_w M_w s_w and the
  * minimum HBM bytes 8 s tau (+ 8 N tau when Y is stored). */
 rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* local_rows, double* macs, double* min_bytes);

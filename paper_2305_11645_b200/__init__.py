@@ -67,7 +67,7 @@ EXPORTS = ["rqmc_plan_create", "rqmc_plan_destroy", "rqmc_strerror", "rqmc_plan_
            "rqmc_plan_summary_get", "rqmc_plan_level", "rqmc_plan_global_row", "rqmc_plan_stats",
            "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_points",
            "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch",
-           "rqmc_plan_summary_batch", "rqmc_plan_dispatch"]
+           "rqmc_plan_summary_batch", "rqmc_plan_dispatch", "rqmc_plan_partition"]
 
 _lib = None
 
@@ -103,6 +103,7 @@ def lib():
         L.rqmc_qn_batch.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), vp, i64,
                                     C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_plan_dispatch.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+        L.rqmc_plan_partition.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
         L.rqmc_profile_read.argtypes = [vp, C.POINTER(C.c_int), dp, dp, dp, dp]
         _lib = L
     return _lib
@@ -177,6 +178,19 @@ class Plan:
         self._check(lib().rqmc_plan_dispatch(self._h, R, f, int(want_y), buf, len(buf)))
         return buf.value.decode()
 
+    def partition(self) -> dict:
+        """Residue classes of this rank: {"classes": ncls, "first": c0, "count": nc}; local row i is
+        global point c0 + (i mod nc) + ncls (i div nc)."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(lib().rqmc_plan_partition(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"classes": a.value, "first": b.value, "count": c.value}
+
+    def global_rows(self):
+        """Global point indices k of this rank's local rows (numpy int64, N_local entries)."""
+        pt = self.partition()
+        i = np.arange(self.summary()["N_local"], dtype=np.int64)
+        return pt["first"] + i % pt["count"] + pt["classes"] * (i // pt["count"])
+
     def global_row(self, i: int) -> int:
         return lib().rqmc_plan_global_row(self._h, i)
 
@@ -211,7 +225,7 @@ class Plan:
         """Y = X A on this rank's rows; with f, also returns the local sum of f (device tensor)."""
         import torch
         self._check_A(A, self.s, self.tau)
-        nl = self.N // self.world
+        nl = self.summary()["N_local"]
         if Y is None:
             Y = torch.empty((nl, self.tau), dtype=torch.float64, device=A.device)
         if fsum is None and f != F_NONE:

@@ -26,7 +26,11 @@ struct GenLevel {
 };
 
 struct GenArgs {
-  int kind, map, b, m, shifted, rank, world, nlev;
+  int kind, map, b, m, shifted, nlev;
+  // residue-class partition: this rank owns classes c0 .. c0+nc-1 of k mod ncls (ncls = b^gamma);
+  // local row l of a level with M >= ncls is global residue c0 + (l mod nc) + ncls (l div nc), of a
+  // level with M < ncls residue (c0 + l) mod M (nc replicated rows)
+  int64_t ncls, c0; int nc;
   double zero_u;                 // u substituted for 0 under Phi^-1 (reading C-5)
   const uint64_t* z;             // lattice z'_j
   const double* shift;           // lattice Delta_j

@@ -68,6 +68,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct rqmc_plan_s {
   int b = 0, m = 0, s = 0, tau = 0, kind = 0, map = 0, rank = 0, world = 1;
+  int64_t ncls = 1, c0 = 0; int nc = 1;   // residue classes k mod ncls; this rank owns [c0, c0 + nc)
   bool shifted = false;
   uint64_t seed = 0;         // reduced MC
   int64_t N = 0, Nl = 0;
@@ -303,15 +304,31 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
   p->N = ipow(d->b, d->m);
   p->world = d->world <= 0 ? 1 : d->world;
   p->rank = d->rank;
-  {  // world must be a power of b dividing N
+  {  // residue-class partition: world a power of b dividing N -> one class per rank;
+     // else ncls = b^gamma (gamma <= m, the smallest with b^gamma >= 32 world) classes in contiguous
+     // groups of floor / ceil(ncls / world) per rank (imbalance <= 1 + world / ncls <= 1.03)
+    if (p->rank < 0 || p->rank >= p->world) {
+      delete p;
+      return bad(RQMC_EINVAL, "need 0 <= rank < world");
+    }
     int64_t g = p->world;
     while (g > 1 && g % p->b == 0) g /= p->b;
-    if (g != 1 || p->N % p->world != 0 || p->rank < 0 || p->rank >= p->world) {
-      delete p;
-      return bad(RQMC_EUNSUPPORTED, "world must be a power of b dividing N and 0 <= rank < world");
+    if (g == 1 && p->N % p->world == 0) {
+      p->ncls = p->world; p->c0 = p->rank; p->nc = 1;
+    } else {
+      int64_t cl = 1;
+      int gam = 0;
+      while (gam < d->m && cl < 32 * (int64_t)p->world) { cl *= p->b; ++gam; }
+      if (cl < p->world) {
+        delete p;
+        return bad(RQMC_EUNSUPPORTED, "world > N: fewer points than ranks");
+      }
+      p->ncls = cl;
+      p->c0 = cl * p->rank / p->world;
+      p->nc = (int)(cl * (p->rank + 1) / p->world - p->c0);
     }
   }
-  p->Nl = p->N / p->world;
+  p->Nl = p->nc * (p->N / p->ncls);
   p->w.assign(d->w, d->w + d->s);
   p->s_star = 0;
   for (int j = 0; j < d->s; ++j)
@@ -397,7 +414,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
         Level L{};
         L.w = wl; L.j_lo = j; L.s_w = j2 - j;
         L.M = ipow(d->b, d->m - wl);
-        L.Ml = L.M >= p->world ? L.M / p->world : 1;
+        L.Ml = L.M >= p->ncls ? p->nc * (L.M / p->ncls) : p->nc;
         fine_to_coarse.push_back(L);
       }
       j = j2;
@@ -461,7 +478,18 @@ rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* o) {
   return RQMC_OK;
 }
 
-int64_t rqmc_plan_global_row(rqmc_plan_t p, int64_t i) { return p ? p->rank + (int64_t)p->world * i : -1; }
+int64_t rqmc_plan_global_row(rqmc_plan_t p, int64_t i) {
+  if (!p || i < 0 || i >= p->Nl) return -1;
+  return p->c0 + i % p->nc + p->ncls * (i / p->nc);
+}
+
+rqmc_status rqmc_plan_partition(rqmc_plan_t p, int64_t* classes, int64_t* first, int64_t* count) {
+  if (!p) return RQMC_EINVAL;
+  if (classes) *classes = p->ncls;
+  if (first) *first = p->c0;
+  if (count) *count = p->nc;
+  return RQMC_OK;
+}
 
 rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* rows, double* macs, double* bytes) {
   if (!p) return RQMC_EINVAL;
@@ -504,7 +532,7 @@ rqmc_status upload(rqmc_plan_s* p) {
 GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
   GenArgs g{};
   g.kind = p->kind; g.map = p->map; g.b = p->b; g.m = p->m; g.shifted = p->shifted;
-  g.rank = p->rank; g.world = p->world; g.nlev = (int)p->lv.size();
+  g.ncls = p->ncls; g.c0 = p->c0; g.nc = p->nc; g.nlev = (int)p->lv.size();
   g.zero_u = p->shifted ? std::ldexp(1.0, -53) : 0.5 / (double)p->N;
   g.seed = p->seed;
   g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds;

@@ -115,7 +115,7 @@ def _oracle(prob):
 def _run_case(rq, prob, X, Yo, tmpl, nf, rank=0, world=1):
     pl = rq.Plan.from_problem(prob, rank=rank, world=world)
     assert pl.summary()["n_fine"] == nf
-    ks = rank + world * np.arange(prob.N // world)
+    ks = pl.global_rows()
     A = torch.from_numpy(prob.A).cuda()
     fp = np.array([0.2, 1.0])
     assert pl.dispatch(W.F_NONE, want_y=True) == f"{tmpl.split('>')[0]}" + (
@@ -159,7 +159,11 @@ def test_fine_path(rq, monkeypatch, cid):
 RANK_CASES = [("tree42", 2, "4", "k_fine_tree<4,2", 4), ("tree62", 4, "6", "k_fine_tree<6,2", 6),
               ("gen3_b2", 4, "3", "k_fine<3,BotB2>", 3), ("gen3_log2", 2, "3", "k_fine<3,BotNone>", 3),
               ("tree33", 3, "3", "k_fine_tree<3,3", 3), ("gen3_b3", 3, "3", "k_fine<3,BotB3>", 3),
-              ("tree42_net", 4, "4", "k_fine_tree<4,2", 4)]
+              ("tree42_net", 4, "4", "k_fine_tree<4,2", 4),
+              # grouped residue classes (world not a power of b: ncls = b^gamma, contiguous groups)
+              ("tree33", 2, "3", "k_fine_tree<3,3", 3), ("tree23", 4, "2", "k_fine_tree<2,3", 2),
+              ("gen3_b3", 8, "3", "k_fine<3,BotB3>", 3), ("tree42", 3, "4", "k_fine_tree<4,2", 4),
+              ("gen2_log2_b3", 2, "2", "k_fine<2,BotNone>", 2)]
 
 
 @pytest.mark.parametrize("cid,G,ck,tmpl,nf", RANK_CASES)

@@ -258,10 +258,12 @@ def test_unaligned_lda_path(rq):
 
 # ------------------------------------------------------------------ multi-rank (simulated on one GPU)
 
-@pytest.mark.parametrize("b,m,G", [(2, 12, 2), (2, 12, 4), (2, 12, 8), (3, 7, 3), (3, 7, 9)])
+@pytest.mark.parametrize("b,m,G", [(2, 12, 2), (2, 12, 4), (2, 12, 8), (3, 7, 3), (3, 7, 9),
+                                   (3, 7, 2), (3, 7, 4), (3, 7, 8), (2, 12, 3), (2, 12, 6)])
 def test_simulated_ranks(rq, b, m, G):
-    """Run plan(rank=g, world=G) for every g on one GPU: local rows are k = g + G i and the sum of
-    the partial f-sums equals the world = 1 result (SURVEY §4 multi-GPU (ii))."""
+    """Run plan(rank=g, world=G) for every g on one GPU: local rows are the rank's residue classes
+    (k = g + G i when G is a power of b, contiguous groups of b^gamma classes otherwise) and the sum
+    of the partial f-sums equals the world = 1 result (SURVEY §4 multi-GPU (ii))."""
     prob = W.make_random(300 + G, b, m, 50, 40, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
     A = dev(prob.A)
     full_p = rq.Plan.from_problem(prob)
@@ -271,7 +273,7 @@ def test_simulated_ranks(rq, b, m, G):
     for g in range(G):
         pg = rq.Plan.from_problem(prob, rank=g, world=G)
         Yg, sg = pg.xa(A, prob.f, prob.fparam)
-        ks = g + G * np.arange(prob.N // G)
+        ks = pg.global_rows()
         np.testing.assert_allclose(Yg.cpu().numpy(), Yf[ks], rtol=0, atol=1e-13 * np.abs(Yf).max())
         tot += float(sg.item())
     assert abs(tot - float(sf.item())) <= 1e-12 * abs(float(sf.item()))
@@ -373,6 +375,28 @@ def test_config_c5_rank_partition(rq):
     del Y
     torch.cuda.empty_cache()
     check_y(prob, Ys, g + G * loc)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_config_c4_grouped_ranks(rq, G):
+    """C4 (b = 3) on G = 2, 4, 8 ranks: ncls = 3^gamma >= 32 G residue classes in contiguous groups
+    (SURVEY §8(e)).  Per rank the fused f-sum of rqmc_xa (Y stored, N_local rows); the G sums add up to
+    the single-GPU sum, and rank G-1's first 64 and 128 seeded local rows match the oracle."""
+    prob = W.make_config("C4")
+    A = dev(prob.A)
+    one = float(rq.Plan.from_problem(prob).qn_sum(A, prob.f, prob.fparam).item())
+    tot = 0.0
+    for g in range(G):
+        pl = rq.Plan.from_problem(prob, rank=g, world=G)
+        Y, fs = pl.xa(A, prob.f, prob.fparam)
+        tot += float(fs.item())
+        if g == G - 1:
+            loc = np.unique(np.concatenate([np.arange(64), np.random.default_rng(G).integers(0, len(Y), 128)]))
+            Ys = Y[torch.from_numpy(loc.astype(np.int64)).cuda()].cpu().numpy()
+            check_y(prob, Ys, pl.global_rows()[loc])
+        del Y
+        torch.cuda.empty_cache()
+    assert abs(tot - one) <= 1e-12 * abs(one), (G, tot, one)
 
 
 def test_config_c5_panel_rows(rq):

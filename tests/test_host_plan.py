@@ -44,7 +44,8 @@ def _plan(rq, **kw):
     (dict(shift=[0.0, 1.0, 0.5, 0.5]), "ESHIFT"),
     (dict(m=40), "EUNSUPPORTED"),
     (dict(m=33), "EUNSUPPORTED"),          # N = 2^33 > 2^32
-    (dict(world=3), "EUNSUPPORTED"),
+    (dict(world=3, rank=3), "EINVAL"),                          # rank outside [0, world)
+    (dict(world=17), "EUNSUPPORTED"),                          # more ranks than points (N = 16)
     (dict(s=0, w=[], z=[]), "EDIM"),
 ])
 def test_validation_codes(rq, kw, code):
@@ -149,6 +150,36 @@ def test_residue_partition_covers_once(rq, b, m, G):
         for L in p.levels():
             assert L["M_local"] == max(L["M"] // G, 1)
     assert np.all(seen == 1)
+
+
+@pytest.mark.parametrize("b,m,G", [(3, 6, 2), (3, 6, 4), (3, 6, 8), (2, 9, 3), (2, 9, 6), (5, 4, 2),
+                                   (3, 12, 8), (3, 3, 5)])
+def test_grouped_partition_covers_once(rq, b, m, G):
+    """world not a power of b (b = 3 on 2/4/8 GPUs, ...): ncls = b^gamma >= 32 G classes (gamma <= m) in
+    contiguous groups per rank; local row i is k = c0 + (i mod nc) + ncls (i div nc).  The ranks cover
+    0..N-1 exactly once, group sizes differ by at most one class, and each level's local rows are
+    nc M / ncls (nc replicated rows when M < ncls)."""
+    s = 2 * m
+    w = W.w_log(b, m, s)
+    z = W.draw_z(3, b, m, w)
+    N = b ** m
+    seen = np.zeros(N, dtype=np.int64)
+    sizes = []
+    for g in range(G):
+        p = rq.Plan(b, m, s, 4, w, z=z, rank=g, world=G)
+        pt = p.partition()
+        ncls, c0, nc = pt["classes"], pt["first"], pt["count"]
+        assert ncls == min(b ** m, next(b ** e for e in range(64) if b ** e >= 32 * G))
+        assert c0 == ncls * g // G and nc == ncls * (g + 1) // G - c0 >= 1
+        sizes.append(nc)
+        ks = p.global_rows()
+        assert len(ks) == p.summary()["N_local"] == nc * (N // ncls)
+        assert all(p.global_row(i) == ks[i] for i in (0, 1, len(ks) - 1))
+        assert np.all((ks % ncls >= c0) & (ks % ncls < c0 + nc))
+        seen[ks] += 1
+        for L in p.levels():
+            assert L["M_local"] == (nc * (L["M"] // ncls) if L["M"] >= ncls else nc)
+    assert np.all(seen == 1) and max(sizes) - min(sizes) <= 1
 
 
 def _gloo_worker(rank, world, port, q):
