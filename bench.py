@@ -195,7 +195,7 @@ def main():
 
     plan = rq.Plan.from_problem(prob, rank=rank, world=world)
     summ = plan.summary()
-    part = plan.partition()
+    partn = plan.partition()
     A = torch.from_numpy(prob.A).cuda()
     fsum = torch.zeros(1, dtype=torch.float64, device="cuda")
     ws = plan.workspace()
@@ -367,7 +367,7 @@ def main():
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": describe(prob), "N": prob.N, "s": prob.s, "tau": prob.tau,
-                   "parallelism": (f"residue classes: {part['classes']} classes k mod {part['classes']}, "
+                   "parallelism": (f"residue classes: {partn['classes']} classes k mod {partn['classes']}, "
                                    f"contiguous groups per rank, {world} ranks ({args.dist_backend})")
                                   if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write, outside the step events)",
