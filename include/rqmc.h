@@ -124,6 +124,8 @@ typedef struct {
   int64_t M_local;  /* rows on this rank: nc M / ncls if M >= ncls, else nc (replicated)       */
   int parent;       /* index of the next coarser non-empty level, -1 for the top               */
   int coarse;       /* 1: materialised per-level GEMM pass; 0: fused into the fine kernel      */
+  int fft;          /* 1: coarse level computed by the FFT product over the unit group of
+                       Z / 2^k (unshifted b = 2 lattices, NEXT-4)   */
 } rqmc_level_info;
 
 typedef struct {

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librqmc.so")
 SOURCES = [os.path.join(CSRC, f) for f in
-           ("rqmc_plan.cpp", "rqmc_gen.cu", "rqmc_gemm.cu", "rqmc_fine.cu", "rqmc_tree.cu")]
+           ("rqmc_plan.cpp", "rqmc_gen.cu", "rqmc_gemm.cu", "rqmc_fine.cu", "rqmc_tree.cu", "rqmc_fft.cu")]
 HEADERS = [os.path.join(CSRC, "rqmc_internal.h"), os.path.join(CSRC, "rqmc_device.cuh"),
            os.path.join(ROOT, "include", "rqmc.h")]
 DEPS = SOURCES + HEADERS

@@ -87,6 +87,23 @@ struct FineArgs {
   int64_t nfull; int nsplit;       // set by the launcher
 };
 
+// NEXT-4: one FFT-product level (rqmc_fft.cu).  Per valuation v (K = k - v >= 3): L = 2^(K-2) = L1 L2,
+// lgL1/lgL2 = log2, p = k - 2 - v bits of e, zoff / hoff = offsets (complex elements) of its block in
+// the data buffer Z (L rows x ldz) and in the H buffer (L entries).
+struct FftV { int L, L1, L2, lgL1, lgL2, p; int64_t zoff, hoff; };
+struct FftArgs {
+  int k, nv, s_w, ncol, ldz, map;
+  double zero_u, inv_M;                         // unshifted zero rule, 2^-k
+  const double* A; int64_t lda;                 // the level's rows of A (A + j_lo lda)
+  const int* jsort; const uint32_t* key; int nplus;  // coordinates sorted by (sigma, bitrev(e_j)); nplus: sigma = +1
+  const uint64_t* z;                            // the level's z'_j
+  double2* Z; double2* H;                       // scratch
+  const double* Rp; int64_t ldp, Mp;            // parent R (nullptr: top level)
+  double* R; int64_t ldr;
+  FftV v[32];
+};
+cudaError_t launch_fft_level(const FftArgs& a, cudaStream_t st);
+
 cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, int nrep, cudaStream_t st);
 cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, uint64_t* words,
                           double* vals, cudaStream_t st);

@@ -26,6 +26,8 @@ namespace {
 
 struct Level {
   int w, j_lo, s_w, parent, coarse;
+  int fft_tab;    // index into rqmc_plan_s::fft (FFT-eligible level, NEXT-4), -1 otherwise
+  int fft;        // layout: this coarse level runs as the FFT product (rqmc_fft.cu) instead of the GEMM
   int fused;      // coarse pair parent: R stays on chip, computed with its child (next level) in one launch
   int64_t M, Ml;
   int ldx;
@@ -42,6 +44,7 @@ struct Layout {
   int ldr = 0;               // row stride of R buffers
   size_t off_x = 0, off_r[2] = {0, 0}, off_part = 0, off_a = 0, off_fsum = 0, total = 0;
   size_t off_split = 0, off_cnt = 0; int64_t split_cap = 0;   // fine-kernel tail split (FineArgs::rscr)
+  size_t off_fz = 0, off_fh = 0;   // FFT levels: complex scratch (data, H) shared by the FFT levels
   int64_t max_gen_entries = 0;
   int fine_smem = 0, fine_as_stride = 0, fine_acc_off = 0, leafruns = 1;
   std::vector<int> fine_xs_off, fine_as_off;
@@ -64,6 +67,37 @@ int64_t gcd64(int64_t a, int64_t b) {
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// NEXT-4 FFT level tables: coordinates of the level sorted by (sigma_j, bitrev_{k-2}(e_j)) where
+// z'_j = sigma_j 5^(e_j) (mod 2^k), k = m - w (rqmc_fft.cu)
+struct FftTab {
+  int k = 0, nplus = 0;
+  std::vector<int> jsort;        // level-relative coordinate indices
+  std::vector<uint32_t> key;
+  size_t dev_j = 0, dev_k = 0;   // element offsets into the plan's device table
+};
+
+// discrete log base 5 in U_{2^k} (k >= 3): the e in [0, 2^(k-2)) with 5^e = z (mod 2^k), z = 1 (mod 4).
+// Bit i of e is fixed modulo 2^(i+3), since 5^(2^i) = 1 + 2^(i+2) (mod 2^(i+3)).
+uint32_t dlog5(uint64_t z, int k) {
+  const uint64_t mask = (1ull << k) - 1;
+  uint64_t p = 1, g = 5;
+  uint32_t e = 0;
+  for (int i = 0; i < k - 2; ++i) {
+    const uint64_t mi = (1ull << (i + 3)) - 1;
+    if ((p & mi) != (z & mi)) { e |= 1u << i; p = (p * g) & mask; }
+    g = (g * g) & mask;
+  }
+  return e;
+}
+
+// FFT-eligible levels (NEXT-4): unshifted base-2 lattice, one process (the FFT computes every row of a
+// level), 3 <= k = m - w <= 18 (FFT lengths L = 2^(k-2-v) <= 2^16 = 256 x 256, two passes)
+constexpr int kFftMinK = 3, kFftMaxK = 18;
+// default rule: the FFT replaces s_w M tau MACs by ~5 M log2 M tau flops plus ~3 passes over its
+// scratch; the GEMM wins below ~64 coordinates per level (RQMC_FFT=1 forces every eligible coarse
+// level, RQMC_FFT=0 disables)
+constexpr int kFftMinS = 64;
+
 }  // namespace
 
 struct rqmc_plan_s {
@@ -77,6 +111,8 @@ struct rqmc_plan_s {
   std::vector<uint64_t> z, C, dshift;
   std::vector<double> shift;
   std::vector<Level> lv;     // coarse -> fine (checkpoint-independent fields)
+  std::vector<FftTab> fft;   // FFT-eligible levels' tables
+  int* d_fft = nullptr;      // device copy: all jsort then all keys
   Layout L1;                 // layout of single runs (and the default workspace)
   std::mutex lay_mu;         // batch layouts (deeper checkpoints when replicas add parallelism)
   std::vector<std::unique_ptr<Layout>> lay_cache;
@@ -104,6 +140,7 @@ struct rqmc_plan_s {
   double* d_shift = nullptr;
   uint64_t* d_C = nullptr;
   uint64_t* d_ds = nullptr;
+  std::vector<int> fft_host; // staging of d_fft
   // phase profiling: 5 events per recorded run
   std::vector<cudaEvent_t> prof_ev;
   int prof_max = 0, prof_runs = 0;
@@ -190,6 +227,11 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   L.nfine = nl - 1 - c;
   L.lv = p.lv;
   for (int i = 0; i < nl; ++i) L.lv[i].coarse = i <= c;
+  static const int fft_mode = [] { const char* e = std::getenv("RQMC_FFT"); return e && *e ? std::atoi(e) : -1; }();
+  for (int i = 0; i < nl; ++i) {
+    Level& V = L.lv[i];
+    V.fft = V.coarse && V.fft_tab >= 0 && fft_mode != 0 && (fft_mode == 1 || V.s_w >= kFftMinS);
+  }
   L.nbundles = (L.lv[c].Ml + kBundle - 1) / kBundle;
   L.fine_smem = fine_smem_bytes(p, c, &L.fine_xs_off, &L.fine_as_off, &L.fine_as_stride, &L.fine_acc_off,
                                 &L.leafruns);
@@ -199,6 +241,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   for (auto& V : L.lv) {
     V.ldx = V.coarse ? (V.s_w + 1) / 2 * 2 : V.s_w;
     V.xoff = (int64_t)(off / sizeof(double));
+    if (V.fft) continue;        // FFT levels need no X^red (their H tables are generated in rqmc_fft.cu)
     off = align_up(off + (size_t)V.Ml * V.ldx * sizeof(double), 256);
     L.max_gen_entries = std::max<int64_t>(L.max_gen_entries, V.Ml * V.ldx);
   }
@@ -212,7 +255,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   for (int i = c - 1; i >= 0 && !no_pair; i -= 2) {
     const Level &P = L.lv[i], &C = L.lv[i + 1];
     const int64_t ncu = C.Ml / P.Ml;
-    if (C.parent == i && ncu * P.Ml == C.Ml && ncu >= 1 && ncu <= 4) L.lv[i].fused = 1;
+    if (C.parent == i && ncu * P.Ml == C.Ml && ncu >= 1 && ncu <= 4 && !P.fft && !C.fft) L.lv[i].fused = 1;
   }
   size_t rsz[2] = {0, 0};
   int nstored = 0;
@@ -232,6 +275,19 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
     L.split_cap = (p.b == 3 && L.nfine > 0 && cap * 8 <= (int64_t(64) << 20)) ? cap : 0;
     L.off_split = off; off = align_up(off + (size_t)L.split_cap * sizeof(double), 256);
     L.off_cnt = off; off = align_up(off + (L.split_cap ? (size_t)kSplitSlots * sizeof(unsigned int) : 0), 256);
+  }
+  {  // FFT scratch: sum_v L_v complex per column (ldz = ldr) and per H, for the largest FFT level
+    size_t zc = 0, hc = 0;
+    for (const Level& V : L.lv)
+      if (V.fft) {
+        const int k = p.m - V.w;
+        size_t sl = 0;
+        for (int v = 0; v <= k - 3; ++v) sl += (size_t)1 << (k - 2 - v);
+        zc = std::max(zc, sl * (size_t)L.ldr);
+        hc = std::max(hc, sl);
+      }
+    L.off_fz = off; off = align_up(off + zc * 2 * sizeof(double), 256);
+    L.off_fh = off; off = align_up(off + hc * 2 * sizeof(double), 256);
   }
   L.off_fsum = off; off = align_up(off + sizeof(double), 256);
   L.off_a = off; off = align_up(off + (size_t)p.s * L.ldr * sizeof(double), 256);
@@ -412,7 +468,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       // (reduced MC: N_j = 1 for w_j >= m -- one i.i.d. draw per coordinate, P:981 N_{s+1} = 1)
       if (wl < d->m || p->shifted || d->map != RQMC_MAP_UNIT || d->kind == RQMC_REDUCED_MC) {
         Level L{};
-        L.w = wl; L.j_lo = j; L.s_w = j2 - j;
+        L.w = wl; L.j_lo = j; L.s_w = j2 - j; L.fft_tab = -1;
         L.M = ipow(d->b, d->m - wl);
         L.Ml = L.M >= p->ncls ? p->nc * (L.M / p->ncls) : p->nc;
         fine_to_coarse.push_back(L);
@@ -423,6 +479,39 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
     for (size_t i = 0; i < p->lv.size(); ++i) p->lv[i].parent = (int)i - 1;
   }
   const int nl = (int)p->lv.size();
+
+  // ---- FFT-eligible levels (NEXT-4, valid without per-coordinate shifts)
+  if (p->kind == RQMC_LATTICE && p->b == 2 && !p->shifted && p->ncls == 1) {
+    for (int i = 0; i < nl; ++i) {
+      Level& V = p->lv[i];
+      const int k = p->m - V.w;
+      if (k < kFftMinK || k > kFftMaxK) continue;
+      FftTab t;
+      t.k = k;
+      std::vector<std::pair<uint64_t, int>> order;   // (sigma- flag << 32 | key, j)
+      for (int q = 0; q < V.s_w; ++q) {
+        const uint64_t zj = p->z[V.j_lo + q] & ((1ull << k) - 1);
+        const bool minus = (zj & 3u) == 3u;
+        const uint64_t z1 = minus ? (((1ull << k) - zj) & ((1ull << k) - 1)) : zj;   // = 1 (mod 4)
+        const uint32_t e = dlog5(z1, k);
+        uint32_t key = 0;
+        for (int b = 0; b < k - 2; ++b) key |= ((e >> b) & 1u) << (k - 3 - b);
+        order.push_back({((uint64_t)minus << 32) | key, q});
+        if (!minus) ++t.nplus;
+      }
+      std::stable_sort(order.begin(), order.end(),
+                       [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (auto& o : order) { t.jsort.push_back(o.second); t.key.push_back((uint32_t)o.first); }
+      V.fft_tab = (int)p->fft.size();
+      p->fft.push_back(std::move(t));
+    }
+    for (auto& t : p->fft) {
+      t.dev_j = p->fft_host.size();
+      p->fft_host.insert(p->fft_host.end(), t.jsort.begin(), t.jsort.end());
+      t.dev_k = p->fft_host.size();
+      for (uint32_t kk : t.key) p->fft_host.push_back((int)kk);
+    }
+  }
 
   // ---- checkpoint and workspace layout of single runs ----
   {
@@ -446,6 +535,7 @@ void rqmc_plan_destroy(rqmc_plan_t p) {
   if (p->d_shift) cudaFree(p->d_shift);
   if (p->d_C) cudaFree(p->d_C);
   if (p->d_ds) cudaFree(p->d_ds);
+  if (p->d_fft) cudaFree(p->d_fft);
   delete p;
 }
 
@@ -474,7 +564,7 @@ rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* o) {
   if (!p || !o || idx < 0 || idx >= (int)p->lv.size()) return RQMC_EINVAL;
   const Level& L = p->lv[idx];
   o->w = L.w; o->j_lo = L.j_lo; o->s_w = L.s_w; o->M = L.M; o->M_local = L.Ml;
-  o->parent = L.parent; o->coarse = p->L1.lv[idx].coarse;
+  o->parent = L.parent; o->coarse = p->L1.lv[idx].coarse; o->fft = p->L1.lv[idx].fft;
   return RQMC_OK;
 }
 
@@ -523,6 +613,7 @@ rqmc_status upload(rqmc_plan_s* p) {
     cp(p->d_shift, p->shift);
     cp(p->d_C, p->C);
     cp(p->d_ds, p->dshift);
+    cp(p->d_fft, p->fft_host);
   });
   if (p->up_err != cudaSuccess)
     return fail(p, RQMC_ECUDA, std::string("device table upload: ") + cudaGetErrorString(p->up_err));
@@ -541,7 +632,7 @@ GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
     const Level& L = lay.lv[i];
     int tcl = 0;
     while (tcl < 5 && (1 << tcl) < L.ldx) ++tcl;
-    g.lv[i] = GenLevel{L.M, L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, tcl, std::ldexp(1.0, -(p->m - L.w))};
+    g.lv[i] = GenLevel{L.M, L.fft ? 0 : L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, tcl, std::ldexp(1.0, -(p->m - L.w))};
   }
   return g;
 }
@@ -549,6 +640,34 @@ GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
 rqmc_status check_cuda(rqmc_plan_s* p, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return RQMC_OK;
   return fail(p, RQMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Arguments of one FFT level (NEXT-4) on workspace w.
+FftArgs fft_args(const rqmc_plan_s* p, const Layout& lay, const Level& L, char* w, const double* dA, int64_t lda,
+                 const double* Rp, int64_t ldp, int64_t Mp, double* R) {
+  const FftTab& t = p->fft[L.fft_tab];
+  FftArgs a{};
+  a.k = t.k; a.nv = t.k - 2; a.s_w = L.s_w; a.ncol = p->tau; a.ldz = lay.ldr; a.map = p->map;
+  a.zero_u = 0.5 / (double)p->N; a.inv_M = std::ldexp(1.0, -t.k);
+  a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda;
+  a.jsort = p->d_fft + t.dev_j; a.key = reinterpret_cast<const uint32_t*>(p->d_fft + t.dev_k); a.nplus = t.nplus;
+  a.z = p->d_z + L.j_lo;
+  a.Z = reinterpret_cast<double2*>(w + lay.off_fz); a.H = reinterpret_cast<double2*>(w + lay.off_fh);
+  a.Rp = Rp; a.ldp = ldp; a.Mp = Mp;
+  a.R = R; a.ldr = lay.ldr;
+  int64_t zo = 0;
+  for (int v = 0; v < a.nv; ++v) {
+    FftV& V = a.v[v];
+    V.p = t.k - 2 - v;
+    V.L = 1 << V.p;
+    V.lgL1 = std::min(V.p, 8);
+    V.lgL2 = V.p - V.lgL1;
+    V.L1 = 1 << V.lgL1; V.L2 = 1 << V.lgL2;
+    V.hoff = zo;
+    V.zoff = zo * lay.ldr;
+    zo += V.L;
+  }
+  return a;
 }
 
 // Arguments of the fused fine kernel for layout `lay` on workspace w (X: X^red base of the slice).
@@ -633,6 +752,12 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
     }
     a.ldr = lay.ldr;
     a.xrep = rep_d; a.rrep = rep_d;
+    if (L.fft) {   // NEXT-4: the level's product by FFTs over the unit group (rqmc_fft.cu); nrep == 1
+      const FftArgs fa = fft_args(p, lay, L, w, dA, lda, a.Rp, a.ldp, a.Mp,
+                                  reinterpret_cast<double*>(w + lay.off_r[L.rbuf]));
+      if (rqmc_status s = check_cuda(p, launch_fft_level(fa, st), "k_fft")) return s;
+      continue;
+    }
     if (L.fused) {
       const Level& Cl = lay.lv[i + 1];
       a.Xc = g.X + Cl.xoff; a.ldxc = Cl.ldx; a.Kc = Cl.s_w; a.Ac = dA + (int64_t)Cl.j_lo * lda;

@@ -209,6 +209,11 @@ def make_config(cfg: str, seed: Optional[int] = None) -> Problem:
     cfg = cfg.upper()
     if cfg.endswith("MC"):
         return as_reduced_mc(make_config(cfg[:-2], seed))
+    if cfg in ("C1U", "C5U"):
+        # NEXT-4 workloads: the config without its random shift (unshifted lattice: every coordinate
+        # of a level has the same map, so the per-level FFT product applies)
+        p = make_config(cfg[:-1], seed)
+        return dataclasses.replace(p, name=cfg, shift=None)
     if cfg == "C3R":
         p = make_config("C3", seed)
         return dataclasses.replace(p, name="C3R", kind=KIND_NET_ROWS,
