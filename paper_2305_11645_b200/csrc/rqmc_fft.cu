@@ -16,15 +16,18 @@
 // 2^(k-1), 2^(k-2), 3 2^(k-2)) are computed directly by the definition (k_fft_rows).  The level's R
 // (R_w[r] = P_w[r] + R_w'[r mod M_w']) is written exactly as the GEMM path writes it.
 //
-// An FFT of length L = L1 L2 (L1 <= 256) is the four-step decomposition over HBM: pass A = FFTs of
-// length L1 across e1 (e = e1 L2 + e2) + twiddles w_L^(e2 f1); pass B = FFTs of length L2 across e2 for
-// each f1 (spectrum f = f1 + L1 f2 stored at f1 L2 + f2).  Three kernels per level:
+// Valuations with L <= 256 run whole in one CTA per column tile (k_fft_small: gather a_v, FFT, multiply
+// by H's spectrum, inverse FFT, scatter).  Longer ones (L = L1 L2, L1, L2 <= 256) use the four-step
+// decomposition over HBM: pass A = FFTs of length L1 across e1 (e = e1 L2 + e2) + twiddles
+// w_L^(e2 f1); pass B = FFTs of length L2 across e2 for each f1 (spectrum f = f1 + L1 f2 stored at
+// f1 L2 + f2):
 //   k_fft_pass1  gather a_v from A's rows (coordinates sorted by (sigma, bit-reversed e_j)) + pass A;
-//                (mode 1: generate H_v instead, one column)
+//                (mode 1: generate H_v instead, one column -- for every valuation)
 //   k_fft_pass2  pass B on the rows f1 and -f1 together, unpack, multiply by H's spectrum, repack,
 //                inverse pass B (mode 1: forward pass B only -> H's spectrum)
 //   k_fft_pass3  inverse pass A, 1/L, unpack P^+, P^-, scatter rows r = 2^v (+-5^e mod 2^K) + parent
-// Each CTA transforms kFftCT = 16 columns (256-byte row segments in HBM) in shared memory, radix 2.
+// In shared memory an FFT of length n <= 256 is itself split n = n1 n2 (n1, n2 <= 16): each thread
+// does a length-n1 then a length-n2 DFT in registers (radix 2, unrolled), one exchange in between.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -33,8 +36,8 @@
 
 namespace rqmc {
 
-constexpr int kFftCT = 16;
 constexpr int kFftThreads = 256;
+constexpr int kFftSmallLg = 8;     // valuations with L <= 2^8 run in k_fft_small
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -44,6 +47,7 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // a conj(b)
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double2 cexpi(int64_t num, int64_t den) {   // exp(-2 pi i num / den)
   double s, c;
   sincospi(-2.0 * (double)num / (double)den, &s, &c);
@@ -69,35 +73,96 @@ __device__ __forceinline__ double fft_phi(const FftArgs& a, uint64_t t) {
   return u;
 }
 
-// twiddles tw[j] = exp(-2 pi i j / n), j < n / 2
+// tw[j] = exp(-2 pi i j / n), j < n
 __device__ __forceinline__ void fft_twiddles(double2* tw, int n) {
-  for (int j = threadIdx.x; j < n / 2; j += blockDim.x) tw[j] = cexpi(j, n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) tw[j] = cexpi(j, n);
 }
 
-// radix-2 DIT over the rows of buf[row * kFftCT + col], n = 2^lg rows stored in bit-reversed order;
-// natural order on return.  inv: conjugate twiddles (unscaled inverse).
-__device__ void fft_rows(double2* buf, int lg, bool inv, const double2* tw) {
-  const int n = 1 << lg;
-  for (int s = 0; s < lg; ++s) {
-    const int h = 1 << s, tsh = lg - 1 - s;   // twiddle index i * n / (2h)
-    for (int idx = threadIdx.x; idx < (n / 2) * kFftCT; idx += blockDim.x) {
-      const int col = idx & (kFftCT - 1), b = idx / kFftCT;
-      const int i = b & (h - 1), r0 = ((b >> s) << (s + 1)) + i, r1 = r0 + h;
-      double2 w = tw[i << tsh];
-      if (inv) w.y = -w.y;
-      const double2 x0 = buf[r0 * kFftCT + col];
-      const double2 t = cmul(w, buf[r1 * kFftCT + col]);
-      buf[r0 * kFftCT + col] = cadd(x0, t);
-      buf[r1 * kFftCT + col] = csub(x0, t);
+// in-register DFT of length N (radix-2 DIT, compile-time indices); twiddle w_N^j = tw[j * ts]
+template <int N, bool INV>
+__device__ __forceinline__ void dft_reg(double2 (&r)[16], const double2* tw, int ts) {
+  constexpr int LG = N <= 1 ? 0 : (N == 2 ? 1 : (N == 4 ? 2 : (N == 8 ? 3 : 4)));
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    int j = 0;
+#pragma unroll
+    for (int b = 0; b < LG; ++b) j |= ((i >> b) & 1) << (LG - 1 - b);
+    if (i < j) { const double2 t = r[i]; r[i] = r[j]; r[j] = t; }
+  }
+#pragma unroll
+  for (int h = 1; h < N; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (i & h) continue;
+      const int jj = i & (h - 1);
+      double2 w = tw[jj * (N / (2 * h)) * ts];
+      if (INV) w.y = -w.y;
+      const double2 t = cmul(w, r[i + h]);
+      r[i + h] = csub(r[i], t);
+      r[i] = cadd(r[i], t);
     }
-    __syncthreads();
+  }
+}
+template <bool INV>
+__device__ __forceinline__ void dft_reg_n(double2 (&r)[16], int lgn, const double2* tw, int ts) {
+  switch (lgn) {
+    case 1: dft_reg<2, INV>(r, tw, ts); break;
+    case 2: dft_reg<4, INV>(r, tw, ts); break;
+    case 3: dft_reg<8, INV>(r, tw, ts); break;
+    case 4: dft_reg<16, INV>(r, tw, ts); break;
+    default: break;
   }
 }
 
-// blockIdx.y -> (v, idx) where valuation v owns cnt(v) consecutive indices
+// FFT of length n = 2^lg (lg <= 8) along the rows of S sequences x CT columns in shared memory,
+// buf[(s n + row) CT + col], natural order in and out; 256 threads = S x CT x (256 / (S CT)) workers.
+// n = n1 n2 (n1 = 2^ceil(lg/2), n2 = 2^floor(lg/2)): worker q < n2 transforms x[i1 n2 + q] over i1 and
+// applies w_n^(q k1); worker q < n1 then transforms over the n2 rows q n2 + i2 into X[q + n1 k2].
+// tw: w_n^j = tw[j tws], j < n.  inv: conjugate twiddles (unscaled).  Ends with a barrier.
+template <int CT, int S, bool INV>
+__device__ void fft_smem(double2* buf, int lg, const double2* tw, int tws = 1) {
+  constexpr int QW = kFftThreads / (S * CT);
+  const int col = threadIdx.x % CT, s = (threadIdx.x / CT) % S, q = threadIdx.x / (CT * S);
+  const int n = 1 << lg, l1 = (lg + 1) >> 1, l2 = lg >> 1, n1 = 1 << l1, n2 = 1 << l2;
+  double2* b = buf + (size_t)s * n * CT + col;
+  double2 r[16];
+  for (int qq = q; qq < n2; qq += QW) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < n1) r[i] = b[(i * n2 + qq) * CT];
+    dft_reg_n<INV>(r, l1, tw, (n / n1) * tws);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < n1) {
+        double2 w = tw[((qq * i) & (n - 1)) * tws];
+        if (INV) w.y = -w.y;
+        b[(i * n2 + qq) * CT] = cmul(r[i], w);
+      }
+  }
+  __syncthreads();
+  if (l2 == 0) return;
+  double2 r2[16];
+  // each worker keeps <= 1 sequence position in registers across the barrier (n1 <= 16 <= QW)
+  const bool act = q < n1;
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < n2) r2[i] = b[(q * n2 + i) * CT];
+    dft_reg_n<INV>(r2, l2, tw, (n / n2) * tws);
+  }
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < n2) b[(q + n1 * i) * CT] = r2[i];
+  }
+  __syncthreads();
+}
+
+// blockIdx.y -> (v, idx) for v in [vlo, vhi) where valuation v owns cnt(v) consecutive indices
 template <class F>
-__device__ __forceinline__ bool fft_task(const FftArgs& a, int y, F cnt, int* v, int* idx) {
-  for (int vv = 0; vv < a.nv; ++vv) {
+__device__ __forceinline__ bool fft_task(const FftArgs& a, int vlo, int vhi, int y, F cnt, int* v, int* idx) {
+  for (int vv = vlo; vv < vhi; ++vv) {
     const int c = cnt(a.v[vv]);
     if (y < c) { *v = vv; *idx = y; return true; }
     y -= c;
@@ -105,207 +170,259 @@ __device__ __forceinline__ bool fft_task(const FftArgs& a, int y, F cnt, int* v,
   return false;
 }
 
-// lower bound of key >= x in keys[lo, hi)
-__device__ __forceinline__ int lbound(const uint32_t* keys, int lo, int hi, uint32_t x) {
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (keys[mid] < x) lo = mid + 1; else hi = mid;
+// a_v(+, e) + i a_v(-, e) for column c (bucket bounds rg[0..3] of (sigma, e mod L), see k_fft_pass1)
+__device__ __forceinline__ double2 fft_gather(const FftArgs& a, const int* rg, int c) {
+  double sp = 0.0, sm = 0.0;
+  for (int q = rg[0]; q < rg[1]; ++q) sp += a.A[(int64_t)a.jsort[q] * a.lda + c];
+  for (int q = rg[2]; q < rg[3]; ++q) sm += a.A[(int64_t)a.jsort[q] * a.lda + c];
+  return make_double2(sp, sm);
+}
+// bucket bounds of e at valuation v: the coordinates are sorted by (sigma, bitrev_{k-2}(e_j)), so the
+// bucket e_j = e (mod 2^p) is the contiguous range of key rev_p(e) (host table FftV::boff: for
+// sigma = +, -, L + 1 range starts in key order)
+__device__ __forceinline__ void fft_bounds(const FftArgs& a, const FftV& V, int e, int* rg) {
+  const int* b = a.boff + V.boff;
+  const int r = brev(e, V.p);
+  rg[0] = b[r]; rg[1] = b[r + 1];
+  rg[2] = b[V.L + 1 + r]; rg[3] = b[V.L + 2 + r];
+}
+// H_v(+, e) + i H_v(-, e)
+__device__ __forceinline__ double2 fft_hval(const FftArgs& a, int vi, int e) {
+  const int K = a.k - vi;
+  const uint32_t mK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
+  const uint32_t u = pow5(e, K);
+  return make_double2(fft_phi(a, (uint64_t)u << vi), fft_phi(a, (uint64_t)((0u - u) & mK) << vi));
+}
+// P^+ + i P^- at f and at -f from the packed spectra Z(f), Z(-f) of a^+- and Hc(f), Hc(-f) of H^+-:
+// a^+(f) = (Z(f) + conj Z(-f)) / 2, a^-(f) = (Z(f) - conj Z(-f)) / 2i (likewise H), spectra at -f
+// are the conjugates (real sequences); P^+ = H^+ conj(a^+) + H^- conj(a^-), P^- = H^- conj(a^+) +
+// H^+ conj(a^-)
+__device__ __forceinline__ void fft_mult(double2 za, double2 zb, double2 ha, double2 hb, double2* wa, double2* wb) {
+  const double2 ap = make_double2(0.5 * (za.x + zb.x), 0.5 * (za.y - zb.y));
+  const double2 am = make_double2(0.5 * (za.y + zb.y), -0.5 * (za.x - zb.x));
+  const double2 hp = make_double2(0.5 * (ha.x + hb.x), 0.5 * (ha.y - hb.y));
+  const double2 hm = make_double2(0.5 * (ha.y + hb.y), -0.5 * (ha.x - hb.x));
+  const double2 Pp = cadd(cmulc(hp, ap), cmulc(hm, am)), Pm = cadd(cmulc(hm, ap), cmulc(hp, am));
+  *wa = make_double2(Pp.x - Pm.y, Pp.y + Pm.x);   // P^+(f) + i P^-(f)
+  *wb = make_double2(Pp.x + Pm.y, Pm.x - Pp.y);   // conj(P^+(f)) + i conj(P^-(f)) = value at -f
+}
+// R[r, c] = P / L + R_parent[r mod M_parent, c] for the rows r = 2^v (+-5^e mod 2^K) of the n entries
+// buf[t] (e = (t / CT) es + e0, column c0 + t % CT); 4 entries per thread in flight (parent loads)
+template <int CT>
+__device__ __forceinline__ void fft_scatter(const FftArgs& a, int vi, const FftV& V, const double2* buf, int e0,
+                                            int es, int n, int c0) {
+  const int K = a.k - vi;
+  const uint32_t mK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
+  const double sc = 1.0 / (double)V.L;
+  for (int t0 = threadIdx.x; t0 < n; t0 += 4 * blockDim.x) {
+    int64_t rp[4], rm[4];
+    double pp[4], pm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x, c = c0 + (t % CT);
+      rp[u] = -1;
+      if (t < n && c < a.ncol) {
+        const uint32_t w5 = pow5((t / CT) * es + e0, K);
+        rp[u] = (int64_t)w5 << vi;
+        rm[u] = (int64_t)((0u - w5) & mK) << vi;
+        pp[u] = a.Rp ? a.Rp[(rp[u] % a.Mp) * a.ldp + c] : 0.0;
+        pm[u] = a.Rp ? a.Rp[(rm[u] % a.Mp) * a.ldp + c] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * blockDim.x, c = c0 + (t % CT);
+      if (rp[u] >= 0) {
+        const double2 x = buf[t];
+        a.R[rp[u] * a.ldr + c] = x.x * sc + pp[u];
+        a.R[rm[u] * a.ldr + c] = x.y * sc + pm[u];
+      }
+    }
   }
-  return lo;
 }
 
-// pass 1: (mode 0) a_v(+-, e) for e = e1 L2 + e2, e1 < L1, packed a^+ + i a^-; (mode 1) H_v(+-, e);
-// FFT over e1; times w_L^(e2 f1); stored at row f1 L2 + e2
-__global__ void __launch_bounds__(kFftThreads) k_fft_pass1(const FftArgs a, int mode) {
+// pass 1 (valuations [vlo, vhi)): (mode 0) a_v for e = e1 L2 + e2, e1 < L1; (mode 1) H_v; FFT over e1;
+// times w_L^(e2 f1); stored at row f1 L2 + e2
+__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass1(const FftArgs a, int mode, int vlo, int vhi) {
   pdl_enter();
+  constexpr int CT = 16;
   int vi, e2;
-  if (!fft_task(a, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
+  if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
   const FftV V = a.v[vi];
-  const int c0 = blockIdx.x * kFftCT;
+  const int c0 = blockIdx.x * CT;
   extern __shared__ __align__(16) double2 fbuf[];
-  double2* buf = fbuf;                       // L1 x kFftCT
-  double2* tw = buf + V.L1 * kFftCT;         // L1 / 2
-  int* rng = reinterpret_cast<int*>(tw + V.L1 / 2 + 1);   // 4 L1 bucket bounds
+  double2* buf = fbuf;                       // L1 x CT
+  double2* tw = buf + V.L1 * CT;             // L1
+  double2* tr = tw + V.L1;                   // row twiddles w_L^(e2 f1), L1
+  int* rng = reinterpret_cast<int*>(tr + V.L1);   // 4 L1 bucket bounds
   fft_twiddles(tw, V.L1);
-  const int K = a.k - vi;
+  for (int f1 = threadIdx.x; f1 < V.L1; f1 += blockDim.x) tr[f1] = cexpi(((int64_t)e2 * f1) & (V.L - 1), V.L);
   if (mode == 0) {
-    // bucket of (sigma, e mod L): keys are e_j bit-reversed over k-2 bits, so e_j = e (mod 2^p)
-    // <-> key in [rev_p(e) << vi, (rev_p(e) + 1) << vi)
-    for (int e1 = threadIdx.x; e1 < V.L1; e1 += blockDim.x) {
-      const int e = e1 * V.L2 + e2;
-      const uint32_t lo = (uint32_t)brev(e, V.p) << vi, hi = lo + (1u << vi);
-      rng[4 * e1 + 0] = lbound(a.key, 0, a.nplus, lo);
-      rng[4 * e1 + 1] = lbound(a.key, 0, a.nplus, hi);
-      rng[4 * e1 + 2] = lbound(a.key, a.nplus, a.s_w, lo);
-      rng[4 * e1 + 3] = lbound(a.key, a.nplus, a.s_w, hi);
-    }
+    for (int e1 = threadIdx.x; e1 < V.L1; e1 += blockDim.x) fft_bounds(a, V, e1 * V.L2 + e2, rng + 4 * e1);
     __syncthreads();
-    for (int t = threadIdx.x; t < V.L1 * kFftCT; t += blockDim.x) {
-      const int e1 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-      double sp = 0.0, sm = 0.0;
-      if (c < a.ncol) {
-        for (int q = rng[4 * e1]; q < rng[4 * e1 + 1]; ++q) sp += a.A[(int64_t)a.jsort[q] * a.lda + c];
-        for (int q = rng[4 * e1 + 2]; q < rng[4 * e1 + 3]; ++q) sm += a.A[(int64_t)a.jsort[q] * a.lda + c];
-      }
-      buf[brev(e1, V.lgL1) * kFftCT + col] = make_double2(sp, sm);
+#pragma unroll 4
+    for (int t = threadIdx.x; t < V.L1 * CT; t += blockDim.x) {
+      const int e1 = t / CT, c = c0 + (t % CT);
+      buf[t] = c < a.ncol ? fft_gather(a, rng + 4 * e1, c) : make_double2(0.0, 0.0);
     }
   } else {
-    const uint32_t mK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
-    for (int t = threadIdx.x; t < V.L1 * kFftCT; t += blockDim.x) {
-      const int e1 = t / kFftCT, col = t & (kFftCT - 1);
-      double2 h = make_double2(0.0, 0.0);
-      if (c0 + col < a.ncol) {
-        const uint32_t u = pow5(e1 * V.L2 + e2, K);
-        h.x = fft_phi(a, (uint64_t)u << vi);
-        h.y = fft_phi(a, (uint64_t)((0u - u) & mK) << vi);
-      }
-      buf[brev(e1, V.lgL1) * kFftCT + col] = h;
+    for (int t = threadIdx.x; t < V.L1 * CT; t += blockDim.x) {
+      const int e1 = t / CT;
+      buf[t] = c0 + (t % CT) < a.ncol ? fft_hval(a, vi, e1 * V.L2 + e2) : make_double2(0.0, 0.0);
     }
   }
   __syncthreads();
-  fft_rows(buf, V.lgL1, false, tw);
-  for (int t = threadIdx.x; t < V.L1 * kFftCT; t += blockDim.x) {
-    const int f1 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-    if (c < a.ncol) {
-      const double2 w = cexpi(((int64_t)e2 * f1) & (V.L - 1), V.L);
-      a.Z[V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c] = cmul(buf[f1 * kFftCT + col], w);
-    }
+  fft_smem<CT, 1, false>(buf, V.lgL1, tw);
+  for (int t = threadIdx.x; t < V.L1 * CT; t += blockDim.x) {
+    const int f1 = t / CT, c = c0 + (t % CT);
+    if (c < a.ncol) a.Z[V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c] = cmul(buf[t], tr[f1]);
   }
 }
 
-// pass 2 on the rows f1 and f1b = -f1 (mod L1): forward FFT over e2 -> f2; (mode 0) unpack a^+-,
-// multiply with H's spectrum, repack P^+ + i P^-, inverse FFT over f2, times conj(w_L^(e2 f1));
+// pass 2 (valuations [vlo, vhi), L2 >= 2) on the rows f1 and f1b = -f1 (mod L1): forward FFT over e2;
+// (mode 0) unpack, multiply with H's spectrum, repack, inverse FFT, times conj(w_L^(e2 f1));
 // (mode 1) store the forward spectrum (H)
-__global__ void __launch_bounds__(kFftThreads) k_fft_pass2(const FftArgs a, int mode) {
+__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass2(const FftArgs a, int mode, int vlo, int vhi) {
   pdl_enter();
+  constexpr int CT = 8;
   int vi, f1;
-  if (!fft_task(a, blockIdx.y, [](const FftV& V) { return V.L1 / 2 + 1; }, &vi, &f1)) return;
+  if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L1 / 2 + 1; }, &vi, &f1)) return;
   const FftV V = a.v[vi];
-  const int c0 = blockIdx.x * kFftCT;
+  const int c0 = blockIdx.x * CT;
   const int f1b = (V.L1 - f1) & (V.L1 - 1);
   const bool two = f1b != f1;
   extern __shared__ __align__(16) double2 fbuf[];
-  double2* b0 = fbuf;
-  double2* b1 = b0 + V.L2 * kFftCT;
-  double2* tw = b1 + V.L2 * kFftCT;
+  double2* b0 = fbuf;                        // sequence 0 (row f1), then sequence 1 (row f1b)
+  double2* b1 = b0 + V.L2 * CT;
+  double2* tw = b1 + V.L2 * CT;              // L2
+  double2* tr = tw + V.L2;                   // 2 L2 row twiddles
   fft_twiddles(tw, V.L2);
+  for (int e2 = threadIdx.x; e2 < V.L2; e2 += blockDim.x) {
+    tr[e2] = cexpi(((int64_t)e2 * f1) & (V.L - 1), V.L);
+    tr[V.L2 + e2] = cexpi(((int64_t)e2 * f1b) & (V.L - 1), V.L);
+  }
   const double2* z0 = a.Z + V.zoff + (int64_t)f1 * V.L2 * a.ldz;
   const double2* z1 = a.Z + V.zoff + (int64_t)f1b * V.L2 * a.ldz;
-  for (int t = threadIdx.x; t < V.L2 * kFftCT; t += blockDim.x) {
-    const int e2 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-    const int d = brev(e2, V.lgL2) * kFftCT + col;
-    b0[d] = c < a.ncol ? z0[(int64_t)e2 * a.ldz + c] : make_double2(0.0, 0.0);
-    if (two) b1[d] = c < a.ncol ? z1[(int64_t)e2 * a.ldz + c] : make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < 2 * V.L2 * CT; t += blockDim.x) {   // all loads in flight (cp.async)
+    const int sq = t / (V.L2 * CT), tt = t - sq * V.L2 * CT, e2 = tt / CT, c = c0 + (tt % CT);
+    const bool ok = c < a.ncol && (sq == 0 || two);
+    cp_async16(b0 + t, ok ? (sq ? z1 : z0) + (int64_t)e2 * a.ldz + c : a.Z, ok);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
-  fft_rows(b0, V.lgL2, false, tw);
-  if (two) fft_rows(b1, V.lgL2, false, tw);
+  fft_smem<CT, 2, false>(b0, V.lgL2, tw);
   if (mode == 1) {
-    for (int t = threadIdx.x; t < V.L2 * kFftCT; t += blockDim.x) {
-      const int f2 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-      if (c < a.ncol) {
-        a.Z[V.zoff + (int64_t)(f1 * V.L2 + f2) * a.ldz + c] = b0[t];
-        if (two) a.Z[V.zoff + (int64_t)(f1b * V.L2 + f2) * a.ldz + c] = b1[t];
-      }
+    for (int t = threadIdx.x; t < 2 * V.L2 * CT; t += blockDim.x) {
+      const int sq = t / (V.L2 * CT), tt = t - sq * V.L2 * CT, f2 = tt / CT, c = c0 + (tt % CT);
+      if (c < a.ncol && (sq == 0 || two)) a.Z[V.zoff + (int64_t)((sq ? f1b : f1) * V.L2 + f2) * a.ldz + c] = b0[t];
     }
     return;
   }
   // pairs {f, -f}: f = f1 + L1 f2 in b0[f2]; -f in (two ? b1 : b0)[f2'], f2' = L2-1-f2 (f1 != 0) or
   // (L2 - f2) mod L2 (f1 = 0).  One thread per unordered pair, results written in place.
   const double2* H = a.H + V.hoff;
-  for (int t = threadIdx.x; t < V.L2 * kFftCT; t += blockDim.x) {
-    const int f2 = t / kFftCT, col = t & (kFftCT - 1);
+  for (int t = threadIdx.x; t < V.L2 * CT; t += blockDim.x) {
+    const int f2 = t / CT, col = t % CT;
     const int f2p = f1 != 0 ? V.L2 - 1 - f2 : ((V.L2 - f2) & (V.L2 - 1));
-    if (!two && f2p < f2) continue;          // the partner's thread handles this pair
-    double2* pa = b0 + f2 * kFftCT + col;
-    double2* pb = (two ? b1 : b0) + f2p * kFftCT + col;
-    const double2 za = *pa, zb = *pb;         // Z(f), Z(-f)
-    const double2 ha = H[f1 * V.L2 + f2], hb = H[f1b * V.L2 + f2p];   // Hc(f), Hc(-f)
-    // a^+(f) = (Z(f) + conj Z(-f)) / 2, a^-(f) = (Z(f) - conj Z(-f)) / 2i; likewise H^+-(f) from Hc
-    const double2 ap = make_double2(0.5 * (za.x + zb.x), 0.5 * (za.y - zb.y));
-    const double2 am = make_double2(0.5 * (za.y + zb.y), -0.5 * (za.x - zb.x));
-    const double2 hp = make_double2(0.5 * (ha.x + hb.x), 0.5 * (ha.y - hb.y));
-    const double2 hm = make_double2(0.5 * (ha.y + hb.y), -0.5 * (ha.x - hb.x));
-    // spectra at -f are the conjugates (real sequences)
-    const double2 apb = make_double2(ap.x, -ap.y), amb = make_double2(am.x, -am.y);
-    const double2 hpb = make_double2(hp.x, -hp.y), hmb = make_double2(hm.x, -hm.y);
-    const double2 Pp = cadd(cmulc(hp, ap), cmulc(hm, am)), Pm = cadd(cmulc(hm, ap), cmulc(hp, am));
-    const double2 Ppb = cadd(cmulc(hpb, apb), cmulc(hmb, amb)), Pmb = cadd(cmulc(hmb, apb), cmulc(hpb, amb));
-    *pa = make_double2(Pp.x - Pm.y, Pp.y + Pm.x);          // P^+ + i P^- at f
-    if (pb != pa) *pb = make_double2(Ppb.x - Pmb.y, Ppb.y + Pmb.x);
+    if (!two && f2p < f2) continue;
+    double2* pa = b0 + f2 * CT + col;
+    double2* pb = (two ? b1 : b0) + f2p * CT + col;
+    double2 wa, wb;
+    fft_mult(*pa, *pb, H[f1 * V.L2 + f2], H[f1b * V.L2 + f2p], &wa, &wb);
+    *pa = wa;
+    if (pb != pa) *pb = wb;
   }
   __syncthreads();
-  // bit-reverse the rows in place, then the inverse FFT over f2
-  for (int t = threadIdx.x; t < V.L2 * kFftCT; t += blockDim.x) {
-    const int i = t / kFftCT, col = t & (kFftCT - 1), j = brev(i, V.lgL2);
-    if (i < j) {
-      double2 x = b0[i * kFftCT + col]; b0[i * kFftCT + col] = b0[j * kFftCT + col]; b0[j * kFftCT + col] = x;
-      if (two) { x = b1[i * kFftCT + col]; b1[i * kFftCT + col] = b1[j * kFftCT + col]; b1[j * kFftCT + col] = x; }
-    }
-  }
-  __syncthreads();
-  fft_rows(b0, V.lgL2, true, tw);
-  if (two) fft_rows(b1, V.lgL2, true, tw);
-  for (int t = threadIdx.x; t < V.L2 * kFftCT; t += blockDim.x) {
-    const int e2 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-    if (c < a.ncol) {
-      double2 w = cexpi(((int64_t)e2 * f1) & (V.L - 1), V.L);
-      w.y = -w.y;
-      a.Z[V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c] = cmul(b0[t], w);
-      if (two) {
-        double2 wb = cexpi(((int64_t)e2 * f1b) & (V.L - 1), V.L);
-        wb.y = -wb.y;
-        a.Z[V.zoff + (int64_t)(f1b * V.L2 + e2) * a.ldz + c] = cmul(b1[t], wb);
-      }
-    }
+  fft_smem<CT, 2, true>(b0, V.lgL2, tw);
+  for (int t = threadIdx.x; t < 2 * V.L2 * CT; t += blockDim.x) {
+    const int sq = t / (V.L2 * CT), tt = t - sq * V.L2 * CT, e2 = tt / CT, c = c0 + (tt % CT);
+    if (c < a.ncol && (sq == 0 || two))
+      a.Z[V.zoff + (int64_t)((sq ? f1b : f1) * V.L2 + e2) * a.ldz + c] = cmul(b0[t], cconj(tr[sq * V.L2 + e2]));
   }
 }
 
-// pass 3: inverse FFT over f1 -> e1, 1/L, P^+ = Re, P^- = Im at e = e1 L2 + e2, rows
-// r = 2^v (+-5^e mod 2^K): R[r, c] = P + R_parent[r mod M_parent, c]
-__global__ void __launch_bounds__(kFftThreads) k_fft_pass3(const FftArgs a) {
+// pass 3 (valuations [vlo, vhi)): inverse FFT over f1 -> e1, 1/L, scatter of P^+ (Re) and P^- (Im)
+// at e = e1 L2 + e2
+__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass3(const FftArgs a, int vlo, int vhi) {
   pdl_enter();
+  constexpr int CT = 16;
   int vi, e2;
-  if (!fft_task(a, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
+  if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
   const FftV V = a.v[vi];
-  const int c0 = blockIdx.x * kFftCT;
+  const int c0 = blockIdx.x * CT;
   extern __shared__ __align__(16) double2 fbuf[];
   double2* buf = fbuf;
-  double2* tw = buf + V.L1 * kFftCT;
-  int64_t* rows = reinterpret_cast<int64_t*>(tw + V.L1 / 2 + 1);   // 2 L1
+  double2* tw = buf + V.L1 * CT;
   fft_twiddles(tw, V.L1);
-  const int K = a.k - vi;
-  const uint32_t mK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
-  for (int e1 = threadIdx.x; e1 < V.L1; e1 += blockDim.x) {
-    const uint32_t u = pow5(e1 * V.L2 + e2, K);
-    rows[2 * e1] = (int64_t)u << vi;
-    rows[2 * e1 + 1] = (int64_t)((0u - u) & mK) << vi;
+  for (int t = threadIdx.x; t < V.L1 * CT; t += blockDim.x) {
+    const int f1 = t / CT, c = c0 + (t % CT);
+    cp_async16(buf + t, c < a.ncol ? a.Z + V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c : a.Z, c < a.ncol);
   }
-  for (int t = threadIdx.x; t < V.L1 * kFftCT; t += blockDim.x) {
-    const int f1 = t / kFftCT, col = t & (kFftCT - 1), c = c0 + col;
-    buf[brev(f1, V.lgL1) * kFftCT + col] =
-        c < a.ncol ? a.Z[V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c] : make_double2(0.0, 0.0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  fft_smem<CT, 1, true>(buf, V.lgL1, tw);
+  fft_scatter<CT>(a, vi, V, buf, e2, V.L2, V.L1 * CT, c0);
+}
+
+// valuations [vlo, nv) with L <= 256 (L2 = 1), all in one CTA per column tile: gather a_vlo, then per
+// valuation FFT, multiply by H's spectrum (natural order: from k_fft_pass1 mode 1), inverse FFT,
+// scatter, and fold a_(v+1)(e) = a_v(e) + a_v(e + L/2) for the next (coarser) valuation
+__global__ void __launch_bounds__(kFftThreads, 1) k_fft_small(const FftArgs a, int vlo) {
+  pdl_enter();
+  constexpr int CT = 16;
+  const FftV V0 = a.v[vlo];
+  const int Ls = V0.L, c0 = blockIdx.x * CT;
+  extern __shared__ __align__(16) double2 fbuf[];
+  double2* acc = fbuf;                       // a_v, Ls x CT
+  double2* buf = acc + Ls * CT;              // work, Ls x CT
+  double2* twL = buf + Ls * CT;              // w_Ls^j, j < Ls
+  double2* tw = twL + Ls;                    // w_L^j of the current valuation (unit stride: constant
+                                             // twiddle offsets in the unrolled sub-DFTs)
+  int* rng = reinterpret_cast<int*>(tw + Ls);
+  fft_twiddles(twL, Ls);
+  for (int e = threadIdx.x; e < Ls; e += blockDim.x) fft_bounds(a, V0, e, rng + 4 * e);
+  __syncthreads();
+#pragma unroll 4
+  for (int t = threadIdx.x; t < Ls * CT; t += blockDim.x) {
+    const int c = c0 + (t % CT);
+    acc[t] = c < a.ncol ? fft_gather(a, rng + 4 * (t / CT), c) : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_rows(buf, V.lgL1, true, tw);
-  const double sc = 1.0 / (double)V.L;
-  for (int t = threadIdx.x; t < 2 * V.L1 * kFftCT; t += blockDim.x) {
-    const int col = t & (kFftCT - 1), q = t / kFftCT, e1 = q >> 1, sg = q & 1, c = c0 + col;
-    if (c >= a.ncol) continue;
-    const double2 x = buf[e1 * kFftCT + col];
-    const int64_t r = rows[2 * e1 + sg];
-    double v = (sg ? x.y : x.x) * sc;
-    if (a.Rp) v += a.Rp[(r % a.Mp) * a.ldp + c];
-    a.R[r * a.ldr + c] = v;
+  for (int vi = vlo; vi < a.nv; ++vi) {
+    const FftV V = a.v[vi];
+    const int n = V.L * CT, tws = Ls / V.L;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) buf[t] = acc[t];
+    for (int j = threadIdx.x; j < V.L; j += blockDim.x) tw[j] = twL[j * tws];
+    __syncthreads();
+    fft_smem<CT, 1, false>(buf, V.p, tw);
+    const double2* H = a.H + V.hoff;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int f = t / CT, col = t % CT, fb = (V.L - f) & (V.L - 1);
+      if (fb < f) continue;
+      double2 wa, wb;
+      fft_mult(buf[f * CT + col], buf[fb * CT + col], H[f], H[fb], &wa, &wb);
+      buf[f * CT + col] = wa;
+      if (fb != f) buf[fb * CT + col] = wb;
+    }
+    __syncthreads();
+    fft_smem<CT, 1, true>(buf, V.p, tw);
+    fft_scatter<CT>(a, vi, V, buf, 0, 1, n, c0);
+    for (int t = threadIdx.x; t < n / 2; t += blockDim.x) acc[t] = cadd(acc[t], acc[t + n / 2]);
+    __syncthreads();
   }
 }
 
 // rows with valuation >= k-2 (0, 2^(k-1), 2^(k-2), 3 2^(k-2)) by the definition: P[r, c] =
-// sum_j phi((r z'_j mod M) / M) A[j, c] in increasing j, plus the parent row
+// sum_j phi((r z'_j mod M) / M) A[j, c], plus the parent row.  CTA = 32 columns x 8 warps; warp w sums
+// j = w (mod 8), the 8 partial sums are added in fixed order.
 __global__ void __launch_bounds__(256) k_fft_rows(const FftArgs a) {
   pdl_enter();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   __shared__ double xs[4][256];
+  __shared__ double red[8][4][32];
   const uint64_t M = 1ull << a.k;
   const uint64_t rr[4] = {0, M >> 1, M >> 2, 3 * (M >> 2)};
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -318,52 +435,61 @@ __global__ void __launch_bounds__(256) k_fft_rows(const FftArgs a) {
     __syncthreads();
     if (c < a.ncol) {
       const int n = min(256, a.s_w - j0);
-      for (int jj = 0; jj < n; ++jj) {
+      for (int jj = warp; jj < n; jj += 8) {
         const double av = a.A[(int64_t)(j0 + jj) * a.lda + c];
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[q] = fma(xs[q][jj], av, acc[q]);
       }
     }
   }
-  if (c < a.ncol) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double v = acc[q];
-      if (a.Rp) v += a.Rp[(int64_t)(rr[q] % (uint64_t)a.Mp) * a.ldp + c];
-      a.R[(int64_t)rr[q] * a.ldr + c] = v;
-    }
+  for (int q = 0; q < 4; ++q) red[warp][q][lane] = acc[q];
+  __syncthreads();
+  if (warp < 4 && c < a.ncol) {
+    const int q = warp;
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][q][lane];
+    if (a.Rp) v += a.Rp[(int64_t)(rr[q] % (uint64_t)a.Mp) * a.ldp + c];
+    a.R[(int64_t)rr[q] * a.ldr + c] = v;
   }
-}
-
-static int fft_smem_bytes(const FftArgs& a, int pass) {
-  int L1 = 1, L2 = 1;
-  for (int i = 0; i < a.nv; ++i) { L1 = max(L1, a.v[i].L1); L2 = max(L2, a.v[i].L2); }
-  if (pass == 2) return (int)sizeof(double2) * (2 * L2 * kFftCT + L2 / 2 + 1);
-  return (int)sizeof(double2) * (L1 * kFftCT + L1 / 2 + 1) + 4 * L1 * (int)sizeof(int64_t);
 }
 
 cudaError_t launch_fft_level(const FftArgs& a0, cudaStream_t st) {
-  int n1 = 0, n2 = 0;
+  // valuations [0, vs) have L > 256 (four-step over HBM), [vs, nv) run in k_fft_small
+  int vs = 0;
+  while (vs < a0.nv && a0.v[vs].p > kFftSmallLg) ++vs;
+  int n1 = 0, n1h = 0, n2 = 0, L1 = 1, L2 = 1, Ls = 1;
   for (int i = 0; i < a0.nv; ++i) {
-    n1 += a0.v[i].L2;
-    n2 += a0.v[i].L1 / 2 + 1;
+    n1h += a0.v[i].L2;
+    if (i < vs) { n1 += a0.v[i].L2; n2 += a0.v[i].L1 / 2 + 1; L1 = max(L1, a0.v[i].L1); L2 = max(L2, a0.v[i].L2); }
+    else Ls = max(Ls, a0.v[i].L);
   }
-  const int s1 = fft_smem_bytes(a0, 1), s2 = fft_smem_bytes(a0, 2);
+  for (int i = vs; i < a0.nv; ++i) L1 = max(L1, a0.v[i].L1);   // pass 1 (mode 1) covers every valuation
+  const int s1 = (int)sizeof(double2) * (L1 * 16 + 2 * L1) + 4 * L1 * (int)sizeof(int);
+  const int s2 = (int)sizeof(double2) * (2 * L2 * 8 + 3 * L2);
+  const int ss = (int)sizeof(double2) * (2 * Ls * 16 + 2 * Ls) + 4 * Ls * (int)sizeof(int);
   cudaError_t e;
   if ((e = set_smem_once(k_fft_pass1, s1)) != cudaSuccess) return e;
   if ((e = set_smem_once(k_fft_pass2, s2)) != cudaSuccess) return e;
   if ((e = set_smem_once(k_fft_pass3, s1)) != cudaSuccess) return e;
-  // H_v and its spectrum (one column), then the data
+  if ((e = set_smem_once(k_fft_small, ss)) != cudaSuccess) return e;
+  // H_v and its spectrum (one column): pass 1 for every valuation, pass 2 for the long ones
   FftArgs h = a0;
   h.Z = a0.H; h.ldz = 1; h.ncol = 1;
   for (int i = 0; i < h.nv; ++i) h.v[i].zoff = h.v[i].hoff;
-  if ((e = launch_k(k_fft_pass1, dim3(1, n1), dim3(kFftThreads), s1, st, true, h, 1)) != cudaSuccess) return e;
-  if ((e = launch_k(k_fft_pass2, dim3(1, n2), dim3(kFftThreads), s2, st, true, h, 1)) != cudaSuccess) return e;
-  const unsigned gx = (unsigned)((a0.ncol + kFftCT - 1) / kFftCT);
-  if ((e = launch_k(k_fft_pass1, dim3(gx, n1), dim3(kFftThreads), s1, st, true, a0, 0)) != cudaSuccess) return e;
-  if ((e = launch_k(k_fft_pass2, dim3(gx, n2), dim3(kFftThreads), s2, st, true, a0, 0)) != cudaSuccess) return e;
-  if ((e = launch_k(k_fft_pass3, dim3(gx, n1), dim3(kFftThreads), s1, st, true, a0)) != cudaSuccess) return e;
-  return launch_k(k_fft_rows, dim3((unsigned)((a0.ncol + 255) / 256)), dim3(256), 0, st, true, a0);
+  if ((e = launch_k(k_fft_pass1, dim3(1, n1h), dim3(kFftThreads), s1, st, true, h, 1, 0, h.nv)) != cudaSuccess) return e;
+  if (vs > 0 && (e = launch_k(k_fft_pass2, dim3(1, n2), dim3(kFftThreads), s2, st, true, h, 1, 0, vs)) != cudaSuccess)
+    return e;
+  const unsigned g16 = (unsigned)((a0.ncol + 15) / 16), g8 = (unsigned)((a0.ncol + 7) / 8);
+  if (vs > 0) {
+    if ((e = launch_k(k_fft_pass1, dim3(g16, n1), dim3(kFftThreads), s1, st, true, a0, 0, 0, vs)) != cudaSuccess) return e;
+    if ((e = launch_k(k_fft_pass2, dim3(g8, n2), dim3(kFftThreads), s2, st, true, a0, 0, 0, vs)) != cudaSuccess) return e;
+    if ((e = launch_k(k_fft_pass3, dim3(g16, n1), dim3(kFftThreads), s1, st, true, a0, 0, vs)) != cudaSuccess) return e;
+  }
+  if (vs < a0.nv && (e = launch_k(k_fft_small, dim3(g16), dim3(kFftThreads), ss, st, true, a0, vs)) != cudaSuccess)
+    return e;
+  return launch_k(k_fft_rows, dim3((unsigned)((a0.ncol + 31) / 32)), dim3(256), 0, st, true, a0);
 }
 
 }  // namespace rqmc

@@ -88,14 +88,15 @@ struct FineArgs {
 };
 
 // NEXT-4: one FFT-product level (rqmc_fft.cu).  Per valuation v (K = k - v >= 3): L = 2^(K-2) = L1 L2,
-// lgL1/lgL2 = log2, p = k - 2 - v bits of e, zoff / hoff = offsets (complex elements) of its block in
-// the data buffer Z (L rows x ldz) and in the H buffer (L entries).
-struct FftV { int L, L1, L2, lgL1, lgL2, p; int64_t zoff, hoff; };
+// lgL1/lgL2 = log2, p = k - 2 - v bits of e, boff = offset of its bucket table (2 (L + 1) starts into
+// jsort: sigma = + then -, in bit-reversed e order), zoff / hoff = offsets (complex elements) of its
+// block in the data buffer Z (L rows x ldz) and in the H buffer (L entries).
+struct FftV { int L, L1, L2, lgL1, lgL2, p, boff; int64_t zoff, hoff; };
 struct FftArgs {
   int k, nv, s_w, ncol, ldz, map;
   double zero_u, inv_M;                         // unshifted zero rule, 2^-k
   const double* A; int64_t lda;                 // the level's rows of A (A + j_lo lda)
-  const int* jsort; const uint32_t* key; int nplus;  // coordinates sorted by (sigma, bitrev(e_j)); nplus: sigma = +1
+  const int* jsort; const int* boff;            // coordinates sorted by (sigma, bitrev(e_j)); bucket starts
   const uint64_t* z;                            // the level's z'_j
   double2* Z; double2* H;                       // scratch
   const double* Rp; int64_t ldp, Mp;            // parent R (nullptr: top level)

@@ -73,6 +73,8 @@ struct FftTab {
   int k = 0, nplus = 0;
   std::vector<int> jsort;        // level-relative coordinate indices
   std::vector<uint32_t> key;
+  std::vector<int> boff;         // per valuation v: 2 (L_v + 1) bucket starts (sigma = +, -)
+  std::vector<int> boff_v;       // offset of valuation v's table in boff
   size_t dev_j = 0, dev_k = 0;   // element offsets into the plan's device table
 };
 
@@ -93,10 +95,12 @@ uint32_t dlog5(uint64_t z, int k) {
 // FFT-eligible levels (NEXT-4): unshifted base-2 lattice, one process (the FFT computes every row of a
 // level), 3 <= k = m - w <= 18 (FFT lengths L = 2^(k-2-v) <= 2^16 = 256 x 256, two passes)
 constexpr int kFftMinK = 3, kFftMaxK = 18;
-// default rule: the FFT replaces s_w M tau MACs by ~5 M log2 M tau flops plus ~3 passes over its
-// scratch; the GEMM wins below ~64 coordinates per level (RQMC_FFT=1 forces every eligible coarse
-// level, RQMC_FFT=0 disables)
-constexpr int kFftMinS = 64;
+// default rule: the FFT replaces s_w M tau MACs by ~5 M log2 M tau flops plus three passes over its
+// scratch (HBM-bound, measured 24-65 ps per R element on C5U: profiles/r02_fft_levels_C5U.txt) while
+// the DMMA GEMM costs ~60 fs per coordinate and element; measured crossover between s_w = 512 and 1024
+// (C5U: w = 11 / 10 FFT 1.1 / 1.6 ms vs GEMM 2.1 ms; w = 9 2.5 vs 2.1 ms).  RQMC_FFT=1 forces every
+// eligible coarse level, RQMC_FFT=0 disables.
+constexpr int kFftMinS = 1024;
 
 }  // namespace
 
@@ -227,7 +231,8 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   L.nfine = nl - 1 - c;
   L.lv = p.lv;
   for (int i = 0; i < nl; ++i) L.lv[i].coarse = i <= c;
-  static const int fft_mode = [] { const char* e = std::getenv("RQMC_FFT"); return e && *e ? std::atoi(e) : -1; }();
+  const char* fe = std::getenv("RQMC_FFT");   // read per plan (tests switch it)
+  const int fft_mode = fe && *fe ? std::atoi(fe) : -1;
   for (int i = 0; i < nl; ++i) {
     Level& V = L.lv[i];
     V.fft = V.coarse && V.fft_tab >= 0 && fft_mode != 0 && (fft_mode == 1 || V.s_w >= kFftMinS);
@@ -502,6 +507,16 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       std::stable_sort(order.begin(), order.end(),
                        [](const auto& x, const auto& y) { return x.first < y.first; });
       for (auto& o : order) { t.jsort.push_back(o.second); t.key.push_back((uint32_t)o.first); }
+      // bucket e (mod 2^p) of valuation v = keys [rho << v, (rho + 1) << v), rho = bitrev_p(e)
+      for (int v = 0; v <= k - 3; ++v) {
+        const int L = 1 << (k - 2 - v);
+        t.boff_v.push_back((int)t.boff.size());
+        for (int sg = 0; sg < 2; ++sg) {
+          const auto b = t.key.begin() + (sg ? t.nplus : 0), e = t.key.begin() + (sg ? V.s_w : t.nplus);
+          for (int rho = 0; rho <= L; ++rho)
+            t.boff.push_back((int)(std::lower_bound(b, e, (uint32_t)rho << v) - t.key.begin()));
+        }
+      }
       V.fft_tab = (int)p->fft.size();
       p->fft.push_back(std::move(t));
     }
@@ -509,7 +524,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       t.dev_j = p->fft_host.size();
       p->fft_host.insert(p->fft_host.end(), t.jsort.begin(), t.jsort.end());
       t.dev_k = p->fft_host.size();
-      for (uint32_t kk : t.key) p->fft_host.push_back((int)kk);
+      p->fft_host.insert(p->fft_host.end(), t.boff.begin(), t.boff.end());
     }
   }
 
@@ -650,7 +665,7 @@ FftArgs fft_args(const rqmc_plan_s* p, const Layout& lay, const Level& L, char* 
   a.k = t.k; a.nv = t.k - 2; a.s_w = L.s_w; a.ncol = p->tau; a.ldz = lay.ldr; a.map = p->map;
   a.zero_u = 0.5 / (double)p->N; a.inv_M = std::ldexp(1.0, -t.k);
   a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda;
-  a.jsort = p->d_fft + t.dev_j; a.key = reinterpret_cast<const uint32_t*>(p->d_fft + t.dev_k); a.nplus = t.nplus;
+  a.jsort = p->d_fft + t.dev_j; a.boff = p->d_fft + t.dev_k;
   a.z = p->d_z + L.j_lo;
   a.Z = reinterpret_cast<double2*>(w + lay.off_fz); a.H = reinterpret_cast<double2*>(w + lay.off_fh);
   a.Rp = Rp; a.ldp = ldp; a.Mp = Mp;
@@ -660,9 +675,10 @@ FftArgs fft_args(const rqmc_plan_s* p, const Layout& lay, const Level& L, char* 
     FftV& V = a.v[v];
     V.p = t.k - 2 - v;
     V.L = 1 << V.p;
-    V.lgL1 = std::min(V.p, 8);
+    V.lgL1 = V.p <= 8 ? V.p : (V.p + 1) / 2;   // L <= 256: one CTA (L2 = 1); else balanced L1 L2
     V.lgL2 = V.p - V.lgL1;
     V.L1 = 1 << V.lgL1; V.L2 = 1 << V.lgL2;
+    V.boff = t.boff_v[v];
     V.hoff = zo;
     V.zoff = zo * lay.ldr;
     zo += V.L;

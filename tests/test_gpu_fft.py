@@ -64,15 +64,18 @@ def test_fft_config_c1(rq, monkeypatch, ck):
     assert abs(float(fs.item()) - q) <= 1e-12 * abs(q)
 
 
-def test_fft_config_c5u(rq):
-    """Unshifted, Phi^-1-mapped C5 shape (C5U) at full size with the default rule (levels w = 6..11,
-    s_w = 64..2048, on the FFT): Q_N over all 2^24 points against the oracle's O3' on every row, and
-    sampled rows of a 64-column panel of Y against the naive oracle; the same plan with the FFT
-    disabled (GEMM levels) agrees."""
+@pytest.mark.parametrize("force", ["", "1"])
+def test_fft_config_c5u(rq, monkeypatch, force):
+    """Unshifted, Phi^-1-mapped C5 shape (C5U) at full size, with the default rule (levels w = 10, 11 on
+    the FFT) and with every coarse level (w = 6..12) forced onto it: Q_N over all 2^24 points against
+    the oracle's O3' on every row, and sampled rows of a 64-column panel of Y against the naive
+    oracle."""
+    monkeypatch.setenv("RQMC_FFT", force)
     prob = W.make_config("C5U")
     pl = rq.Plan.from_problem(prob)
     lv = pl.levels()
-    assert [L["w"] for L in lv if L["fft"]] == [11, 10, 9, 8, 7, 6]
+    exp = [11, 10] if not force else [12, 11, 10, 9, 8, 7, 6]
+    assert [L["w"] for L in lv if L["fft"]] == exp                # default rule: s_w >= 1024
     A = dev(prob.A)
     fs = float(pl.qn_sum(A, prob.f, prob.fparam).item())
     q = oracle.neumaier(oracle.f_all_meanid_tab(prob))
