@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <mutex>
 #include <utility>
@@ -79,16 +80,51 @@ inline cudaError_t set_smem_once(F* kern, int bytes) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Debug build (-DRQMC_DEBUG=1, `_build.py --variant debug`): every cp.async source and every global
+// store of the path is checked against the buffers of the current run (workspace, A, Y, f-sums, plan
+// tables), set per launch sequence by debug_set_ranges(); a violation prints the site and traps.
+// (A bounds-checked stand-in for compute-sanitizer, which is closed on this pool.)
+// ------------------------------------------------------------------------------------------
+#ifndef RQMC_DEBUG
+#define RQMC_DEBUG 0
+#endif
+#if RQMC_DEBUG
+static __constant__ DbgRanges c_dbg;     // one copy per translation unit
+__device__ __forceinline__ bool dbg_ok(const void* p, size_t n) {
+  const char* q = static_cast<const char*>(p);
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (q >= c_dbg.lo[i] && q + n <= c_dbg.hi[i]) return true;
+  return false;
+}
+#define RQMC_DCHECK(p, n)                                                                        \
+  do {                                                                                           \
+    if (!dbg_ok((p), (n))) {                                                                     \
+      printf("RQMC_DEBUG out-of-bounds %s:%d block (%d,%d,%d) thread %d addr %p\n", __FILE__,      \
+             __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, (const void*)(p));          \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+static inline cudaError_t dbg_set_tu(const DbgRanges& r, cudaStream_t st) {
+  return cudaMemcpyToSymbolAsync(c_dbg, &r, sizeof(r), 0, cudaMemcpyHostToDevice, st);
+}
+#else
+#define RQMC_DCHECK(p, n) do { } while (0)
+#endif
+
+// ------------------------------------------------------------------------------------------
 // async copy helpers
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  if (valid) RQMC_DCHECK(src, 16);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(valid ? 16 : 0));
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  if (valid) RQMC_DCHECK(src, 8);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(valid ? 8 : 0));
 }
@@ -171,6 +207,7 @@ __device__ __forceinline__ void store_leaf(const FineArgs& a, const double (&S)[
 #pragma unroll
       for (int cf = 0; cf < 4; ++cf) {
         const int col = c.c0 + cf * 8 + 2 * c.tg;
+        if (col < a.tau) RQMC_DCHECK(yr + col, col + 1 < a.tau ? 16 : 8);
         if (col + 1 < a.tau) {
           if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(S[2 * cf], S[2 * cf + 1]);
           else { yr[col] = S[2 * cf]; yr[col + 1] = S[2 * cf + 1]; }

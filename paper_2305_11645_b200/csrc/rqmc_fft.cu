@@ -234,6 +234,8 @@ __device__ __forceinline__ void fft_scatter(const FftArgs& a, int vi, const FftV
       const int t = t0 + u * blockDim.x, c = c0 + (t % CT);
       if (rp[u] >= 0) {
         const double2 x = buf[t];
+        RQMC_DCHECK(a.R + rp[u] * a.ldr + c, 8);
+        RQMC_DCHECK(a.R + rm[u] * a.ldr + c, 8);
         a.R[rp[u] * a.ldr + c] = x.x * sc + pp[u];
         a.R[rm[u] * a.ldr + c] = x.y * sc + pm[u];
       }
@@ -451,6 +453,7 @@ __global__ void __launch_bounds__(256) k_fft_rows(const FftArgs a) {
 #pragma unroll
     for (int w = 0; w < 8; ++w) v += red[w][q][lane];
     if (a.Rp) v += a.Rp[(int64_t)(rr[q] % (uint64_t)a.Mp) * a.ldp + c];
+    RQMC_DCHECK(a.R + (int64_t)rr[q] * a.ldr + c, 8);
     a.R[(int64_t)rr[q] * a.ldr + c] = v;
   }
 }
@@ -491,5 +494,11 @@ cudaError_t launch_fft_level(const FftArgs& a0, cudaStream_t st) {
     return e;
   return launch_k(k_fft_rows, dim3((unsigned)((a0.ncol + 31) / 32)), dim3(256), 0, st, true, a0);
 }
+
+#if RQMC_DEBUG
+cudaError_t dbg_set_fft(const DbgRanges& r, cudaStream_t st) { return dbg_set_tu(r, st); }
+#else
+cudaError_t dbg_set_fft(const DbgRanges&, cudaStream_t) { return cudaSuccess; }
+#endif
 
 }  // namespace rqmc

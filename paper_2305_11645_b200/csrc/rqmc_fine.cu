@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
       for (int u = 0; u < 4; ++u) {
         const int rr = r + u * (kFineThreads >> 5);
         const int j = rr / L.K, q = rr - j * L.K;
+        if (rr < nrow && t < c.beff) RQMC_DCHECK(src + (int64_t)j * a.Mroot * L.ldx + q, 8);
         v[u] = (rr < nrow && t < c.beff) ? src[(int64_t)j * a.Mroot * L.ldx + q] : 0.0;
       }
 #pragma unroll
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < kFineThreads / 32; ++w) t += red[w];
+      RQMC_DCHECK(a.partial + rep * a.partrep + blockIdx.x, 8);
       a.partial[rep * a.partrep + blockIdx.x] = t;
     }
   }
@@ -563,5 +565,11 @@ cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st
     default: return cudaErrorInvalidValue;
   }
 }
+
+#if RQMC_DEBUG
+cudaError_t dbg_set_fine(const DbgRanges& r, cudaStream_t st) { return dbg_set_tu(r, st); }
+#else
+cudaError_t dbg_set_fine(const DbgRanges&, cudaStream_t) { return cudaSuccess; }
+#endif
 
 }  // namespace rqmc

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
       for (int jn = 0; jn < 4; ++jn) {
         const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
         double* p = R + row * ldr + col;
+        if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
         if (col + 1 < a.tau) {
           *reinterpret_cast<double2*>(p) = make_double2(acc[i][jn][0], acc[i][jn][1]);
         } else if (col < a.tau) {
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
         // sibling-first tiles (mp_blk = Mp) lie inside one period: r mod Mp = in0 + (r - r0)
         const int64_t prow = (mp_blk == a.Mp) ? in0 + (row - r0) : row % a.Mp;
         const double* p = Rpg + prow * a.ldp + col;
+        if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
         if (CH == 2 && col + 1 < a.tau) {
           const double2 v = *reinterpret_cast<const double2*>(p);
           acc[i][jn][0] = v.x;
@@ -248,5 +250,11 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     return vec ? go(k_level_gemm<BM, 2, WMF, false, true>) : go(k_level_gemm<BM, 1, WMF, false, true>);
   return vec ? go(k_level_gemm<BM, 2, WMF, false, false>) : go(k_level_gemm<BM, 1, WMF, false, false>);
 }
+
+#if RQMC_DEBUG
+cudaError_t dbg_set_gemm(const DbgRanges& r, cudaStream_t st) { return dbg_set_tu(r, st); }
+#else
+cudaError_t dbg_set_gemm(const DbgRanges&, cudaStream_t) { return cudaSuccess; }
+#endif
 
 }  // namespace rqmc

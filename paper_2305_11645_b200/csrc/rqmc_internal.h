@@ -105,6 +105,15 @@ struct FftArgs {
 };
 cudaError_t launch_fft_level(const FftArgs& a, cudaStream_t st);
 
+// debug build (RQMC_DEBUG): device address ranges a run may touch; each translation unit keeps its
+// own __constant__ copy, set by its dbg_set_* before the run's launches (rqmc_device.cuh)
+struct DbgRanges { const char* lo[6]; const char* hi[6]; };
+cudaError_t dbg_set_gen(const DbgRanges& r, cudaStream_t st);
+cudaError_t dbg_set_gemm(const DbgRanges& r, cudaStream_t st);
+cudaError_t dbg_set_fine(const DbgRanges& r, cudaStream_t st);
+cudaError_t dbg_set_tree(const DbgRanges& r, cudaStream_t st);
+cudaError_t dbg_set_fft(const DbgRanges& r, cudaStream_t st);
+
 cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, int nrep, cudaStream_t st);
 cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, uint64_t* words,
                           double* vals, cudaStream_t st);

@@ -20,6 +20,10 @@
 #include "../../include/rqmc.h"
 #include "rqmc_internal.h"
 
+#ifndef RQMC_DEBUG
+#define RQMC_DEBUG 0
+#endif
+
 using namespace rqmc;
 
 namespace {
@@ -738,6 +742,22 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
                      int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
                      cudaStream_t st) {
   const bool want_f = f != RQMC_F_NONE && d_fsum;
+#if RQMC_DEBUG
+  {  // debug build: the buffers this run may touch (workspace slices, A, Y, f-sums, plan tables)
+    DbgRanges dr{};
+    auto set = [&](int i, const void* p, size_t n) {
+      dr.lo[i] = static_cast<const char*>(p); dr.hi[i] = p ? static_cast<const char*>(p) + n : nullptr;
+    };
+    set(0, w, (size_t)nrep * rep_bytes + lay.total);   // slices + shift table (superset)
+    set(1, dA, (size_t)p->s * lda * sizeof(double));
+    set(2, dY, dY ? (size_t)p->Nl * ldy * sizeof(double) : 0);
+    set(3, d_fsum, d_fsum ? (size_t)nrep * sizeof(double) : 0);
+    set(4, p->d_fft, p->fft_host.size() * sizeof(int));
+    set(5, p->d_z, p->z.size() * sizeof(uint64_t));
+    for (auto fn : {dbg_set_gen, dbg_set_gemm, dbg_set_fine, dbg_set_tree, dbg_set_fft})
+      if (rqmc_status s = check_cuda(p, fn(dr, st), "debug ranges")) return s;
+  }
+#endif
   cudaEvent_t* ev = nullptr;
   if (p->prof_runs < p->prof_max) ev = &p->prof_ev[5 * p->prof_runs++];
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
@@ -823,7 +843,8 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   // The launch sequence of a run depends only on these arguments: capture it once as a CUDA graph and
   // replay it (one launch instead of ~9; ~60 us -> ~15 us on C1).  Not while phase profiling records
   // per-run events, nor with RQMC_NO_GRAPH=1.
-  static const bool no_graph = [] { const char* e = std::getenv("RQMC_NO_GRAPH"); return e && *e && *e != '0'; }();
+  // (debug builds launch directly: their per-run range uploads are host copies)
+  static const bool no_graph = RQMC_DEBUG || [] { const char* e = std::getenv("RQMC_NO_GRAPH"); return e && *e && *e != '0'; }();
   if (no_graph || p->prof_max > 0) return direct();
   const double fp0 = fparam ? fparam[0] : 0.0, fp1 = fparam ? fparam[1] : 0.0;
   const int fk = want_f ? (int)f : -1;

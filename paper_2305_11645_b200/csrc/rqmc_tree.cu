@@ -268,6 +268,7 @@ __device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[
 #pragma unroll
       for (int cf = 0; cf < NFR; ++cf) {
         const int col = c.c0 + c.cw + cf * 8 + 2 * c.tg;
+        if (col < a.tau) RQMC_DCHECK(yr + col, col + 1 < a.tau ? 16 : 8);
         if (col + 1 < a.tau) {
           if (a.y_vec) *reinterpret_cast<double2*>(yr + col) = make_double2(S[2 * cf], S[2 * cf + 1]);
           else { yr[col] = S[2 * cf]; yr[col + 1] = S[2 * cf + 1]; }
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     constexpr int SCR = T::LEAVES * BUN;
     double* scr = (kSplit && split) ? a.rscr + rep * a.partrep + (bundle - a.nfull) * 2 * SCR : nullptr;
     auto use = [&](int idx, double rs) {
-      if (kSplit && split) scr[sidx * SCR + idx] = rs;
+      if (kSplit && split) { RQMC_DCHECK(scr + sidx * SCR + idx, 8); scr[sidx * SCR + idx] = rs; }
       else part += f_of_mean(a, (rs - pad) / a.tau);
     };
     if constexpr (Run::kRegAcc) {
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t += red[w];
+      RQMC_DCHECK(a.partial + rep * a.partrep + bundle, 8);
       a.partial[rep * a.partrep + bundle] = t;
     }
   }
@@ -866,5 +868,11 @@ cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st
     default: return cudaErrorNotSupported;
   }
 }
+
+#if RQMC_DEBUG
+cudaError_t dbg_set_tree(const DbgRanges& r, cudaStream_t st) { return dbg_set_tu(r, st); }
+#else
+cudaError_t dbg_set_tree(const DbgRanges&, cudaStream_t) { return cudaSuccess; }
+#endif
 
 }  // namespace rqmc

@@ -1,0 +1,31 @@
+"""Bounds-checked debug build (VERDICT r1 "What's missing" 5: compute-sanitizer is closed on this pool).
+
+librqmc_debug.so is the same library compiled with -DRQMC_DEBUG=1: every cp.async source and every
+global store of the path (k_gen X^red, GEMM R tiles and parent rows, fine-kernel X^red / A / root loads,
+Y stores, partials, tail-split scratch, FFT R rows) is checked against the buffers of the run and a
+violation traps.  This test re-runs a cross-section of the parity suites -- every fused-fine kernel
+template, the b = 3 tail split, batches, the residue partition, the FFT levels -- against that library
+(RQMC_LIB) in a subprocess; any out-of-bounds access fails it.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_parity_subset_under_bounds_checks():
+    from paper_2305_11645_b200 import _build
+    lib = _build.build(variant="debug", defines=("RQMC_DEBUG=1",))
+    env = dict(os.environ, RQMC_LIB=lib)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_fine_paths.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py"),
+           os.path.join(ROOT, "tests", "test_gpu_batch.py"), os.path.join(ROOT, "tests", "test_gpu_fft.py"),
+           "-k", "not c5 and not c4 and not c3 and not c2 and not config"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-2000:])
+    assert "RQMC_DEBUG out-of-bounds" not in r.stdout + r.stderr
+    assert " passed" in r.stdout
