@@ -628,6 +628,10 @@ rqmc_status upload(rqmc_plan_s* p) {
       p->up_err = cudaMalloc((void**)&dst, n);
       if (p->up_err == cudaSuccess) p->up_err = cudaMemcpy(dst, src.data(), n, cudaMemcpyHostToDevice);
     };
+#if RQMC_DEBUG
+    // the bounds checks spill the largest trees to a ~1.3 KB stack frame (above the 1 KB default)
+    if (p->up_err == cudaSuccess) p->up_err = cudaDeviceSetLimit(cudaLimitStackSize, 4096);
+#endif
     cp(p->d_z, p->z);
     cp(p->d_shift, p->shift);
     cp(p->d_C, p->C);

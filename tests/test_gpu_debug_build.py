@@ -24,8 +24,11 @@ def test_parity_subset_under_bounds_checks():
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
            os.path.join(ROOT, "tests", "test_gpu_fine_paths.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py"),
            os.path.join(ROOT, "tests", "test_gpu_batch.py"), os.path.join(ROOT, "tests", "test_gpu_fft.py"),
-           "-k", "not c5 and not c4 and not c3 and not c2 and not config"]
+           "-k", "not config and not qn_host and not pair_fusion"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "debug_build_run.log"), "w") as fh:
+        fh.write(r.stdout + "\n" + r.stderr)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-2000:])
     assert "RQMC_DEBUG out-of-bounds" not in r.stdout + r.stderr
     assert " passed" in r.stdout
