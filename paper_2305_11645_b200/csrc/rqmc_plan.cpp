@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
+
 #include "../../include/rqmc.h"
 #include "rqmc_internal.h"
 
@@ -70,6 +72,18 @@ int64_t gcd64(int64_t a, int64_t b) {
   return a;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// NVTX range per phase of a run (host-side markers; free when no tool is attached).  During CUDA-graph
+// capture they mark the captured sequence once.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+struct NvtxPhase {            // consecutive phases: next() closes the previous range
+  bool open = false;
+  void next(const char* name) { if (open) nvtxRangePop(); nvtxRangePushA(name); open = true; }
+  ~NvtxPhase() { if (open) nvtxRangePop(); }
+};
 
 // NEXT-4 FFT level tables: coordinates of the level sorted by (sigma_j, bitrev_{k-2}(e_j)) where
 // z'_j = sigma_j 5^(e_j) (mod 2^k), k = m - w (rqmc_fft.cu)
@@ -767,6 +781,9 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
   const int64_t rep_d = (int64_t)(rep_bytes / sizeof(double));
   mark(0);
+  NvtxRange r_run("rqmc:run");
+  NvtxPhase phase;
+  phase.next("rqmc:a2 points (k_gen)");
 
   // a2: reduced points of every level (all replicas: grid.z)
   GenArgs g = gen_args(p, lay, w);
@@ -776,6 +793,7 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
+  phase.next("rqmc:a3+a4 coarse levels (k_level_gemm / k_fft)");
   if (a_ready)
     if (rqmc_status s = check_cuda(p, cudaStreamWaitEvent(st, a_ready, 0), "wait for A")) return s;
 
@@ -811,6 +829,7 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   }
 
   mark(2);
+  phase.next("rqmc:a3-a5 fused fine levels + f (k_fine, k_reduce)");
 
   // a3+a4+a5 fine levels fused with f / Y store
   const FineArgs fa = fine_args(p, lay, w, g.X, dA, lda, dY, ldy, want_f ? (int)f : -1, fparam, rep_d);
