@@ -199,11 +199,18 @@ __device__ __forceinline__ double f_of_mean(const FineArgs& a, double mean) {
   }
 }
 
+// Y row of local leaf row l (identity, or the residue chunk's row map, FineArgs::ym_nc)
+__device__ __forceinline__ int64_t y_row(const FineArgs& a, int64_t l) {
+  if (a.ym_nc == 0) return l;
+  const int64_t q = l / a.ym_nc;
+  return a.ym_c0 + (l - q * a.ym_nc) + a.ym_ncls * q;
+}
+
 template <bool STY>
 __device__ __forceinline__ void store_leaf(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
   if constexpr (STY) {
     if (c.t < c.beff) {
-      double* yr = a.Y + (c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+      double* yr = a.Y + y_row(a, c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
 #pragma unroll
       for (int cf = 0; cf < 4; ++cf) {
         const int col = c.c0 + cf * 8 + 2 * c.tg;

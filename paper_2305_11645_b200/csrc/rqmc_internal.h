@@ -85,6 +85,9 @@ struct FineArgs {
   double* rscr; int64_t rscr_cap;  // scratch (doubles per replica slice)
   unsigned int* rcnt; int ncnt;    // counters per replica slice (stride 2 partrep)
   int64_t nfull; int nsplit;       // set by the launcher
+  // Y row map of a residue chunk (rqmc_plan.cpp, chunked xa): local row l is stored at global row
+  // ym_c0 + (l mod ym_nc) + ym_ncls (l div ym_nc); ym_nc = 0: row l
+  int64_t ym_c0, ym_ncls; int ym_nc;
 };
 
 // NEXT-4: one FFT-product level (rqmc_fft.cu).  Per valuation v (K = k - v >= 3): L = 2^(K-2) = L1 L2,

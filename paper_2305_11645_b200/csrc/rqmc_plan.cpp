@@ -163,6 +163,15 @@ struct rqmc_plan_s {
   uint64_t* d_C = nullptr;
   uint64_t* d_ds = nullptr;
   std::vector<int> fft_host; // staging of d_fft
+  // residue-chunk pipeline of rqmc_xa (Y stored, one process): sub-plans over contiguous groups of
+  // the residue classes k mod chunk_ncls, whose coarse GEMMs (main stream) overlap the previous
+  // chunk's HBM-bound fine kernel (side stream)
+  std::vector<std::unique_ptr<rqmc_plan_s>> chunks;
+  std::vector<size_t> chunk_off;       // workspace offset of each chunk's slice
+  size_t chunk_sums = 0, chunk_total = 0;
+  int64_t chunk_ncls = 0;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
   // phase profiling: 5 events per recorded run
   std::vector<cudaEvent_t> prof_ev;
   int prof_max = 0, prof_runs = 0;
@@ -329,6 +338,56 @@ const Layout& layout_for(rqmc_plan_s* p, int64_t reps, int f) {
   p->lay_cache.emplace_back(new Layout());
   make_layout(*p, c, *p->lay_cache.back());
   return *p->lay_cache.back();
+}
+
+// Residue-chunk pipeline for rqmc_xa (Y stored): the N x tau Y stream makes the fine kernel HBM-bound
+// while the coarse GEMMs are fp64-bound, so splitting the problem into nchunk groups of the residue
+// classes k mod ncls (ncls = the smallest coarse level M >= 8 nchunk; every subtree under one residue
+// is independent) lets chunk i+1's coarse GEMMs overlap chunk i's fine kernel.  Each
+// chunk is a sub-plan with the same levels and checkpoint and local rows c0 + (l mod nc) + ncls (l div
+// nc); its fine kernel stores those rows of the caller's Y directly.  Y is bit-identical to the
+// unchunked run (the same per-row arithmetic); the f-sum is the fixed-order sum of the chunk sums.
+// Only for one process (world = 1), Y >= 2 GB (N tau >= 2^28), no FFT levels; RQMC_CHUNKS=n sets the
+// chunk count (default 4; 0 or 1 disables).
+void make_chunks(rqmc_plan_s* p) {
+  const char* e = std::getenv("RQMC_CHUNKS");
+  const int nch = e && *e ? std::atoi(e) : 4;
+#if RQMC_DEBUG
+  (void)nch;
+  return;   // debug builds set their bounds per launch sequence on one stream
+#else
+  if (nch < 2 || p->world != 1 || p->ncls != 1 || (double)p->N * p->tau < (double)(1ull << 28)) return;
+  const Layout& L = p->L1;
+  for (int i = 0; i <= L.ckpt; ++i)
+    if (L.lv[i].fft) return;
+  int64_t ncls = 0;
+  for (int i = 0; i <= L.ckpt; ++i)
+    if (L.lv[i].M >= 8 * nch && (ncls == 0 || L.lv[i].M < ncls)) ncls = L.lv[i].M;
+  if (ncls == 0) return;
+  size_t off = 0;
+  for (int c = 0; c < nch; ++c) {
+    std::unique_ptr<rqmc_plan_s> q(new rqmc_plan_s());
+    q->b = p->b; q->m = p->m; q->s = p->s; q->tau = p->tau; q->kind = p->kind; q->map = p->map;
+    q->shifted = p->shifted; q->seed = p->seed; q->N = p->N; q->s_star = p->s_star;
+    q->w = p->w; q->z = p->z; q->C = p->C; q->dshift = p->dshift; q->shift = p->shift;
+    q->ncls = ncls;
+    q->c0 = ncls * c / nch;
+    q->nc = (int)(ncls * (c + 1) / nch - q->c0);
+    q->Nl = q->nc * (p->N / ncls);
+    q->lv = p->lv;
+    for (Level& V : q->lv) {
+      V.Ml = V.M >= ncls ? q->nc * (V.M / ncls) : q->nc;
+      V.fft_tab = -1;
+    }
+    make_layout(*q, L.ckpt, q->L1);
+    p->chunk_off.push_back(off);
+    off = align_up(off + q->L1.total, 256);
+    p->chunks.push_back(std::move(q));
+  }
+  p->chunk_sums = off;
+  p->chunk_total = align_up(off + nch * sizeof(double), 256);
+  p->chunk_ncls = ncls;
+#endif
 }
 
 }  // namespace
@@ -552,6 +611,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
     if (c < 0) { delete p; return bad(RQMC_EUNSUPPORTED, "no feasible checkpoint level"); }
     make_layout(*p, c, p->L1);
   }
+  make_chunks(p);
   *out = p;
   return RQMC_OK;
 }
@@ -569,6 +629,8 @@ void rqmc_plan_destroy(rqmc_plan_t p) {
   if (p->d_C) cudaFree(p->d_C);
   if (p->d_ds) cudaFree(p->d_ds);
   if (p->d_fft) cudaFree(p->d_fft);
+  for (auto e : p->chunk_ev) cudaEventDestroy(e);
+  if (p->side) cudaStreamDestroy(p->side);
   delete p;
 }
 
@@ -626,7 +688,7 @@ rqmc_status rqmc_plan_stats(rqmc_plan_t p, int want_y, int64_t* rows, double* ma
 
 rqmc_status rqmc_workspace_size(rqmc_plan_t p, size_t* bytes) {
   if (!p || !bytes) return RQMC_EINVAL;
-  *bytes = p->L1.total;
+  *bytes = std::max(p->L1.total, p->chunk_total);
   return RQMC_OK;
 }
 
@@ -654,6 +716,8 @@ rqmc_status upload(rqmc_plan_s* p) {
   });
   if (p->up_err != cudaSuccess)
     return fail(p, RQMC_ECUDA, std::string("device table upload: ") + cudaGetErrorString(p->up_err));
+  for (auto& q : p->chunks)
+    if (rqmc_status s = upload(q.get())) return fail(p, s, q->err);
   return RQMC_OK;
 }
 
@@ -754,14 +818,23 @@ struct RunRand {
   int srep;
 };
 
+// A residue chunk of a chunked rqmc_xa: the fine kernel and its reduction run on fine_st after the
+// chunk's coarse levels (event ev), storing the chunk's rows of the caller's Y (row map).
+struct ChunkCtx {
+  cudaStream_t fine_st;
+  cudaEvent_t ev;
+  int64_t ym_c0, ym_ncls;
+  int ym_nc;
+};
+
 rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_t rep_bytes, const RunRand& rr,
                      cudaEvent_t a_ready /* nullable: A is produced on another stream; wait before the GEMMs */,
                      const double* dA,
                      int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
-                     cudaStream_t st) {
+                     cudaStream_t st, const ChunkCtx* cx = nullptr) {
   const bool want_f = f != RQMC_F_NONE && d_fsum;
 #if RQMC_DEBUG
-  {  // debug build: the buffers this run may touch (workspace slices, A, Y, f-sums, plan tables)
+  if (!cx) {  // debug build: the buffers this run may touch (workspace slices, A, Y, f-sums, plan tables)
     DbgRanges dr{};
     auto set = [&](int i, const void* p, size_t n) {
       dr.lo[i] = static_cast<const char*>(p); dr.hi[i] = p ? static_cast<const char*>(p) + n : nullptr;
@@ -832,7 +905,14 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   phase.next("rqmc:a3-a5 fused fine levels + f (k_fine, k_reduce)");
 
   // a3+a4+a5 fine levels fused with f / Y store
-  const FineArgs fa = fine_args(p, lay, w, g.X, dA, lda, dY, ldy, want_f ? (int)f : -1, fparam, rep_d);
+  FineArgs fa = fine_args(p, lay, w, g.X, dA, lda, dY, ldy, want_f ? (int)f : -1, fparam, rep_d);
+  if (cx) {   // chunk: continue on the fine stream once the coarse levels are done
+    fa.ym_c0 = cx->ym_c0; fa.ym_ncls = cx->ym_ncls; fa.ym_nc = cx->ym_nc;
+    cudaError_t e = cudaEventRecord(cx->ev, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cx->fine_st, cx->ev, 0);
+    if (rqmc_status s = check_cuda(p, e, "chunk fork")) return s;
+    st = cx->fine_st;
+  }
   int64_t nparts = 0;
   if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st, &nparts), "k_fine")) return s;
   mark(3);
@@ -840,6 +920,40 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
     if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, nparts, rep_d, nrep, d_fsum, st), "k_reduce"))
       return s;
   mark(4);
+  return RQMC_OK;
+}
+
+// Chunked rqmc_xa (make_chunks): chunk i's points and coarse levels on st, its fine kernel (and f
+// partial reduction into the chunk sums) on the plan's side stream after them; the side stream joins
+// st at the end, and one fixed-order reduction adds the chunk sums.
+rqmc_status run_chunked(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                        const double* fparam, double* d_fsum, char* w, cudaStream_t st) {
+  const int n = (int)p->chunks.size();
+  cudaError_t e = cudaSuccess;
+  if (!p->side) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, lo);   // lowest: coarse GEMMs first
+    p->chunk_ev.resize(n + 1);
+    for (int i = 0; i <= n && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&p->chunk_ev[i], cudaEventDisableTiming);
+    if (rqmc_status s = check_cuda(p, e, "chunk streams")) return s;
+  }
+  const bool want_f = f != RQMC_F_NONE && d_fsum;
+  double* sums = reinterpret_cast<double*>(w + p->chunk_sums);
+  for (int i = 0; i < n; ++i) {
+    rqmc_plan_s* q = p->chunks[i].get();
+    const ChunkCtx cx{p->side, p->chunk_ev[i], q->c0, q->ncls, q->nc};
+    const RunRand rr{q->d_shift, q->d_ds, nullptr, 0};
+    if (rqmc_status s = run_core(q, q->L1, 1, w + p->chunk_off[i], q->L1.off_fsum, rr, nullptr, dA, lda, dY, ldy, f,
+                                 fparam, want_f ? sums + i : nullptr, st, &cx))
+      return fail(p, s, q->err);
+  }
+  e = cudaEventRecord(p->chunk_ev[n], p->side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->chunk_ev[n], 0);
+  if (rqmc_status s = check_cuda(p, e, "chunk join")) return s;
+  if (want_f)
+    if (rqmc_status s = check_cuda(p, launch_reduce(sums, n, 0, 1, d_fsum, st), "k_reduce (chunks)")) return s;
   return RQMC_OK;
 }
 
@@ -859,7 +973,11 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   if (!want_f && !dY) return RQMC_OK;
   if (rqmc_status s = upload(p)) return s;
   const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
+  const bool chunked = dY != nullptr && !p->chunks.empty() && p->prof_max == 0;
+  if (chunked && wbytes < p->chunk_total)
+    return fail(p, RQMC_EINVAL, "workspace too small: need " + std::to_string(p->chunk_total));
   auto direct = [&] {
+    if (chunked) return run_chunked(p, dA, lda, dY, ldy, f, fparam, d_fsum, static_cast<char*>(dwork), st);
     return run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, nullptr, dA, lda, dY, ldy, f, fparam,
                     d_fsum, st);
   };
@@ -884,8 +1002,10 @@ rqmc_status run(rqmc_plan_s* p, const double* dA, int64_t lda, double* dY, int64
   // the capture stream starts after earlier work on st (the graph itself is launched on st)
   e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return direct();
-  const rqmc_status s = run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, nullptr, dA, lda, dY, ldy,
-                                 f, fparam, d_fsum, p->cap_stream);
+  const rqmc_status s =
+      chunked ? run_chunked(p, dA, lda, dY, ldy, f, fparam, d_fsum, static_cast<char*>(dwork), p->cap_stream)
+              : run_core(p, p->L1, 1, static_cast<char*>(dwork), p->L1.off_fsum, rr, nullptr, dA, lda, dY, ldy, f,
+                         fparam, d_fsum, p->cap_stream);
   cudaGraph_t graph = nullptr;
   e = cudaStreamEndCapture(p->cap_stream, &graph);
   cudaGraphExec_t exec = nullptr;

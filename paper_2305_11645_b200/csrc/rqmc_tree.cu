@@ -264,7 +264,7 @@ template <bool STY, int NFR>
 __device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[2 * NFR], int j, const TreeCtx& c) {
   if constexpr (STY) {
     if (c.t < c.beff) {
-      double* yr = a.Y + (c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+      double* yr = a.Y + y_row(a, c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
 #pragma unroll
       for (int cf = 0; cf < NFR; ++cf) {
         const int col = c.c0 + c.cw + cf * 8 + 2 * c.tg;
