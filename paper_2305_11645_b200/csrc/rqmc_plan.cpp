@@ -347,11 +347,14 @@ const Layout& layout_for(rqmc_plan_s* p, int64_t reps, int f) {
 // chunk is a sub-plan with the same levels and checkpoint and local rows c0 + (l mod nc) + ncls (l div
 // nc); its fine kernel stores those rows of the caller's Y directly.  Y is bit-identical to the
 // unchunked run (the same per-row arithmetic); the f-sum is the fixed-order sum of the chunk sums.
-// Only for one process (world = 1), Y >= 2 GB (N tau >= 2^28), no FFT levels; RQMC_CHUNKS=n sets the
-// chunk count (default 4; 0 or 1 disables).
+// Only for one process (world = 1), Y >= 2 GB (N tau >= 2^28), no FFT levels.  OPT-IN (RQMC_CHUNKS=n,
+// n >= 2): measured slower on C4 (4.52 ms unchunked; 2 / 4 / 8 chunks 5.49 / 5.96 / 7.08 ms): a chunk's
+// fine grid is 1.4 waves (638 CTAs on 444 slots, 1.16 ms vs 3.29 / 4 = 0.82), and the fine kernel
+// holds every SM, so the next chunk's GEMMs barely overlap it (serialised kernel sum 6.39 ms vs 5.96 ms
+// wall; profiles/r02_c4_chunks.txt).
 void make_chunks(rqmc_plan_s* p) {
   const char* e = std::getenv("RQMC_CHUNKS");
-  const int nch = e && *e ? std::atoi(e) : 4;
+  const int nch = e && *e ? std::atoi(e) : 0;
 #if RQMC_DEBUG
   (void)nch;
   return;   // debug builds set their bounds per launch sequence on one stream
