@@ -1,6 +1,8 @@
 // a3+a4 coarse level GEMM (k_level_gemm): one level of paper Alg. 2,
 // R_w = tile(R_w') + X^red_w A_w, as a DMMA.8x8x4 (fp64 tensor core) GEMM -- optionally fused with
 // the next finer level (R_c = tile(R_w) + X^red_c A_c) so that R_w never goes to HBM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -205,6 +207,177 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// TMA variant (RQMC_GEMM_TMA=1; north_star "tiles of A staged through TMA and shared memory"): the
+// X^red tile (64 rows x 16 k) and the A tile (16 k x 64 columns, four 16 x 16 boxes) of each k-tile are
+// brought in by cp.async.bulk.tensor with 128-byte swizzle, completing on one mbarrier per stage
+// (3-stage ring, thread 0 issues); the 4 warps read the DMMA fragments through the swizzle.  Same
+// arithmetic and k order as k_level_gemm (bit-identical R).  Single replica, K % 16 == 0, 16-byte
+// aligned A / lda even, 64-row slices.
+// ------------------------------------------------------------------------------------------
+constexpr int kTmaStages = 3;
+constexpr int kTmaStageBytes = 64 * 16 * 8 + 4 * 16 * 16 * 8;   // X tile + 4 A boxes = 16 KB
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int WMF>
+__global__ void __launch_bounds__(128) k_level_gemm_tma(const GemmArgs a, const __grid_constant__ CUtensorMap tmX,
+                                                         const __grid_constant__ CUtensorMap tmA, int64_t mp_blk,
+                                                         int64_t nu, int64_t y0) {
+  pdl_enter();
+  constexpr int BM = 64, BN = 64, BK = 16, NST = kTmaStages, WR = 8 * WMF;
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t bar[NST];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / 2, wn = warp % 2, g = lane >> 2, tg = lane & 3;
+  const int64_t yb = y0 + blockIdx.y;
+  const int64_t pb = (int64_t)((uint32_t)yb / (uint32_t)nu), u = yb - pb * nu;
+  const int64_t in0 = pb * BM, r0 = u * mp_blk + in0;
+  const int64_t rlim = min(a.M, u * mp_blk + mp_blk);
+  const int c0 = blockIdx.x * BN;
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm) + 1023) & ~uintptr_t(1023));
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nk = a.K / BK;
+  auto issue = [&](int kt) {   // thread 0: stage kt's X tile and A boxes
+    unsigned char* sb = base + (kt % NST) * kTmaStageBytes;
+    uint64_t* b = &bar[kt % NST];
+    mbar_expect_tx(b, kTmaStageBytes);
+    tma_load_2d(sb, &tmX, kt * BK, (int)r0, b);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(sb + 8192 + q * 2048, &tmA, c0 + 16 * q, kt * BK, b);
+  };
+  if (tid == 0)
+    for (int s = 0; s < NST - 1 && s < nk; ++s) issue(s);
+
+  double acc[WMF][4][2];
+#pragma unroll
+  for (int i = 0; i < WMF; ++i) {
+    const int64_t row = r0 + wm * WR + i * 8 + g;
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) {
+      const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
+      acc[i][jn][0] = 0.0;
+      acc[i][jn][1] = 0.0;
+      if (a.Rp && row < rlim) {
+        const int64_t prow = (mp_blk == a.Mp) ? in0 + (row - r0) : row % a.Mp;
+        const double* p = a.Rp + prow * a.ldp + col;
+        if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
+        if (col + 1 < a.tau) {
+          const double2 v = *reinterpret_cast<const double2*>(p);
+          acc[i][jn][0] = v.x;
+          acc[i][jn][1] = v.y;
+        } else if (col < a.tau) {
+          acc[i][jn][0] = p[0];
+        }
+      }
+    }
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    mbar_wait(&bar[kt % NST], (unsigned)((kt / NST) & 1));
+    __syncthreads();   // every warp is past stage kt-1: its buffer may be refilled
+    if (tid == 0 && kt + NST - 1 < nk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(kt + NST - 1);
+    }
+    const unsigned char* sx = base + (kt % NST) * kTmaStageBytes;
+    const unsigned char* sa = sx + 8192;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int k = kk + tg;
+      double af[WMF], bf[4];
+#pragma unroll
+      for (int i = 0; i < WMF; ++i) {   // X[row][k], row & 7 = g: 128-byte swizzle XORs the 16-byte chunk
+        const int row = wm * WR + i * 8 + g;
+        const int off = row * 128 + ((((k >> 1) ^ g) & 7) << 4) + ((k & 1) << 3);
+        af[i] = *reinterpret_cast<const double*>(sx + off);
+      }
+#pragma unroll
+      for (int jn = 0; jn < 4; ++jn) {  // A[k][col] in box col / 16, row k
+        const int col = wn * 32 + jn * 8 + g, c16 = col & 15;
+        const int off = (col >> 4) * 2048 + k * 128 + ((((c16 >> 1) ^ k) & 7) << 4) + ((c16 & 1) << 3);
+        bf[jn] = *reinterpret_cast<const double*>(sa + off);
+      }
+#pragma unroll
+      for (int i = 0; i < WMF; ++i)
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) dmma(acc[i][jn], af[i], bf[jn]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < WMF; ++i) {
+    const int64_t row = r0 + wm * WR + i * 8 + g;
+    if (row >= rlim) continue;
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) {
+      const int col = c0 + wn * 32 + jn * 8 + 2 * tg;
+      double* p = a.R + row * a.ldr + col;
+      if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
+      if (col + 1 < a.tau) {
+        *reinterpret_cast<double2*>(p) = make_double2(acc[i][jn][0], acc[i][jn][1]);
+      } else if (col < a.tau) {
+        p[0] = acc[i][jn][0];
+      }
+    }
+  }
+}
+
+// 2-D tensor map of a row-major fp64 matrix (rows x cols, leading dimension ld), box bc x br, 128-byte
+// swizzle, out-of-bounds elements read as zero
+static bool make_tmap(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld, int bc, int br) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static cudaError_t launch_gemm_tma(const GemmArgs& a, int64_t mp_blk, int64_t nu, int64_t nrb, cudaStream_t st) {
+  CUtensorMap tx, ta;
+  if (!make_tmap(&tx, a.X, a.M, a.ldx, a.ldx, 16, 64) || !make_tmap(&ta, a.A, a.K, a.tau, a.lda, 16, 16))
+    return cudaErrorNotSupported;
+  constexpr int WMF = 4;
+  const int sm = kTmaStages * kTmaStageBytes + 1024;
+  cudaError_t e = set_smem_once(k_level_gemm_tma<WMF>, sm);
+  if (e != cudaSuccess) return e;
+  for (int64_t y0 = 0; y0 < nrb; y0 += 65535) {
+    dim3 grid((unsigned)((a.tau + 63) / 64), (unsigned)std::min<int64_t>(65535, nrb - y0), 1);
+    if ((e = launch_k(k_level_gemm_tma<WMF>, grid, dim3(128), sm, st, true, a, tx, ta, mp_blk, nu, y0)) != cudaSuccess)
+      return e;
+  }
+  return cudaSuccess;
+}
+
 template <int BM>
 static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st);
 
@@ -233,6 +406,13 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     nu = (a.M + a.Mp - 1) / a.Mp;
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
+  static const bool use_tma = [] { const char* e = std::getenv("RQMC_GEMM_TMA"); return e && *e && *e != '0'; }();
+  if (use_tma && BM == 64 && !pair && vec && nrep == 1 && a.K % 16 == 0 && mp_blk % 64 == 0 && a.ldx % 2 == 0 &&
+      a.M < (int64_t(1) << 31) &&
+      (uintptr_t)a.X % 16 == 0) {
+    const cudaError_t e = launch_gemm_tma(a, mp_blk, nu, nrb, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const int sm = gemm_smem_bytes<BM>();
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = set_smem_once(kern, sm);
