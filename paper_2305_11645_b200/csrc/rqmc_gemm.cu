@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
 }
 
 // ------------------------------------------------------------------------------------------
-// TMA variant (RQMC_GEMM_TMA=1; north_star "tiles of A staged through TMA and shared memory"): the
+// TMA variant (levels with K >= 128; north_star "tiles of A staged through TMA and shared memory"): the
 // X^red tile (64 rows x 16 k) and the A tile (16 k x 64 columns, four 16 x 16 boxes) of each k-tile are
 // brought in by cp.async.bulk.tensor with 128-byte swizzle, completing on one mbarrier per stage
 // (3-stage ring, thread 0 issues); the 4 warps read the DMMA fragments through the swizzle.  Same
@@ -406,7 +406,13 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     nu = (a.M + a.Mp - 1) / a.Mp;
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
-  static const bool use_tma = [] { const char* e = std::getenv("RQMC_GEMM_TMA"); return e && *e && *e != '0'; }();
+  // TMA tiles for K >= 128 (C5 levels 7..11: 2.01-2.07 vs 2.07-2.10 ms, tensor pipe 93.5-94.7 % vs
+  // 91.2-91.8 %: the 128-byte swizzle leaves 2-way bank conflicts on the 8-byte fragment loads
+  // (l1tex wavefronts x2), but the loader's address arithmetic disappears (-18 % instructions)); the
+  // K = 64 level (4 k-tiles, R-traffic bound) is faster on cp.async (2.18 vs 2.28 ms;
+  // profiles/r02_gemm_tma_C5.txt).  RQMC_GEMM_TMA=0 disables, =1 forces every eligible level.
+  static const int tma_mode = [] { const char* e = std::getenv("RQMC_GEMM_TMA"); return e && *e ? std::atoi(e) : -1; }();
+  const bool use_tma = tma_mode == 1 || (tma_mode < 0 && a.K >= 128);
   if (use_tma && BM == 64 && !pair && vec && nrep == 1 && a.K % 16 == 0 && mp_blk % 64 == 0 && a.ldx % 2 == 0 &&
       a.M < (int64_t(1) << 31) &&
       (uintptr_t)a.X % 16 == 0) {
