@@ -412,7 +412,10 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
   // K = 64 level (4 k-tiles, R-traffic bound) is faster on cp.async (2.18 vs 2.28 ms;
   // profiles/r02_gemm_tma_C5.txt).  RQMC_GEMM_TMA=0 disables, =1 forces every eligible level.
   static const int tma_mode = [] { const char* e = std::getenv("RQMC_GEMM_TMA"); return e && *e ? std::atoi(e) : -1; }();
-  const bool use_tma = tma_mode == 1 || (tma_mode < 0 && a.K >= 128);
+  // (and at least one full wave of 592 CTAs: on small grids the 3-stage TMA prologue is exposed, C2's
+  // K = 128 level 12.6 us vs ~9 us)
+  const int64_t ncta = nrb * ((a.tau + 63) / 64);
+  const bool use_tma = tma_mode == 1 || (tma_mode < 0 && a.K >= 128 && ncta >= 592);
   if (use_tma && BM == 64 && !pair && vec && nrep == 1 && a.K % 16 == 0 && mp_blk % 64 == 0 && a.ldx % 2 == 0 &&
       a.M < (int64_t(1) << 31) &&
       (uintptr_t)a.X % 16 == 0) {
