@@ -160,6 +160,7 @@ constexpr int kPad = kFinePad;
 struct FineCtx {
   int grp, wm, g, tg, t, beff, c0;
   int64_t r0;
+  int64_t ybase, ystride;  // Y row of this lane's residue (leaf run 0) and the step per leaf run
   const double* as;      // A slab of the current column tile
 };
 
@@ -199,18 +200,22 @@ __device__ __forceinline__ double f_of_mean(const FineArgs& a, double mean) {
   }
 }
 
-// Y row of local leaf row l (identity, or the residue chunk's row map, FineArgs::ym_nc)
+// Y row of local row l (identity, or the residue chunk's row map, FineArgs::ym_nc) and the Y row step
+// per leaf run (see FineArgs::ym_nc): evaluated once per thread
 __device__ __forceinline__ int64_t y_row(const FineArgs& a, int64_t l) {
   if (a.ym_nc == 0) return l;
   const int64_t q = l / a.ym_nc;
   return a.ym_c0 + (l - q * a.ym_nc) + a.ym_ncls * q;
+}
+__device__ __forceinline__ int64_t y_stride(const FineArgs& a) {
+  return a.ym_nc == 0 ? a.Mroot : a.ym_ncls * (a.Mroot / a.ym_nc);
 }
 
 template <bool STY>
 __device__ __forceinline__ void store_leaf(const FineArgs& a, const double (&S)[8], int j, const FineCtx& c) {
   if constexpr (STY) {
     if (c.t < c.beff) {
-      double* yr = a.Y + y_row(a, c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+      double* yr = a.Y + (c.ybase + (int64_t)j * c.ystride) * a.ldy;
 #pragma unroll
       for (int cf = 0; cf < 4; ++cf) {
         const int col = c.c0 + cf * 8 + 2 * c.tg;

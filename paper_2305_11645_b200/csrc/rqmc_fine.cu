@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
   const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
   const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
   c.beff = (int)((a.Mroot - c.r0) < kBundle ? (a.Mroot - c.r0) : kBundle);
+  c.ybase = y_row(a, c.r0 + c.t);
+  c.ystride = y_stride(a);
 
   // X^red of the subtree -> smem [run][q][t] (t stride kPad); global rows r0 + t + j Mroot, read
   // row-contiguously, written transposed.

@@ -10,6 +10,8 @@ namespace rqmc {
 
 constexpr int kMaxLevels = 64;
 constexpr int kMaxFine = 7;       // fused fine levels (compile-time DFS depth; 8 never fits the smem bound)
+constexpr int kFineSlots = 8;     // FineArgs::lv entries (kept at 8: the kernels' parameter layout with 8
+                                  // slots lets ptxas allocate the C5 tree without spills)
 constexpr int kBundle = 32;       // residues of the checkpoint level per fine CTA
 constexpr int kSplitSlots = 512;  // max tail bundles split over two CTAs (FineArgs::rscr)
 constexpr int kFineBN = 32;       // column tile of the fine kernel
@@ -68,7 +70,7 @@ struct FineLevel {
 struct FineArgs {
   const double* root; int64_t ldroot; int64_t Mroot;
   int NF;
-  FineLevel lv[kMaxFine];
+  FineLevel lv[kFineSlots];
   const double* A; int64_t lda; int tau; int a_vec;  // a_vec: 16B cp.async allowed
   double* Y; int64_t ldy; int y_vec;  // y_vec: 16B stores allowed
   int fk; double fp0, fp1;
@@ -86,7 +88,9 @@ struct FineArgs {
   unsigned int* rcnt; int ncnt;    // counters per replica slice (stride 2 partrep)
   int64_t nfull; int nsplit;       // set by the launcher
   // Y row map of a residue chunk (rqmc_plan.cpp, chunked xa): local row l is stored at global row
-  // ym_c0 + (l mod ym_nc) + ym_ncls (l div ym_nc); ym_nc = 0: row l
+  // ym_c0 + (l mod ym_nc) + ym_ncls (l div ym_nc); ym_nc = 0: row l.  Leaf rows of one residue are
+  // l = r + j Mroot (Mroot a multiple of ym_nc), i.e. global rows y_row(r) + j ystride with
+  // ystride = Mroot (ym_nc = 0) or ym_ncls Mroot / ym_nc: the kernels map once per thread.
   int64_t ym_c0, ym_ncls; int ym_nc;
 };
 

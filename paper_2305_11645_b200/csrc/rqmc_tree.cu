@@ -94,6 +94,7 @@ struct Tree {
 struct TreeCtx {
   int grp, ch, wm, g, tg, t, cw, beff, c0;
   int64_t r0;
+  int64_t ybase, ystride;  // Y row of this lane's residue (leaf run 0) and the step per leaf run
   const double* as;  // A slab of the current column tile
 };
 
@@ -213,13 +214,14 @@ __device__ __constant__ static const double kExp2Tab64[64] = {
     1.978456026387951
 };
 
-// exp(x) for the elementwise g = exp(p0 y) of C2 (|x| <= 700; NaN, +-inf and |x| > 700 go to libdevice
-// exp, so overflow / underflow / NaN propagate exactly as in the general kernel): x = (k/64) ln 2 + r with
+// exp(x) for the elementwise g = exp(p0 y) of C2: x = (k/64) ln 2 + r with
 // |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
 // (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
 // exponent field.  11 fp64 instructions + 1 LDS vs 16 fp64 + branch for exp(); <= ~2.5 ulp.
-__device__ __forceinline__ double exp_t(double x, const double* etab) {
-  if (__builtin_expect(!(fabs(x) <= 700.0), 0)) return exp(x);
+// Out of range by predicated selects (no branch): x > 709.78 -> +inf (overflow), x < -708.39 -> 0 (the
+// subnormal range is flushed: absolute error < 2.3e-308), NaN -> NaN.
+__device__ __forceinline__ double exp_t(double x0, const double* etab) {
+  const double x = fmin(fmax(x0, -708.0), 709.0);
   const double kd = rint(x * 92.33248261689366);                 // 64 / ln 2
   double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
   r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
@@ -230,7 +232,10 @@ __device__ __forceinline__ double exp_t(double x, const double* etab) {
   p = fma(p, r, 1.0);
   const int k = (int)kd;
   const double v = etab[k & 63] * p;
-  return __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
+  double e = __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
+  e = x0 > 709.782712893384 ? __longlong_as_double(0x7ff0000000000000ll) : e;
+  e = x0 < -708.3964185322641 ? 0.0 : e;
+  return x0 != x0 ? x0 : e;
 }
 
 // lane-local sum of g over one leaf node's NV values (reading C-17: 1 identity, 2 exp(p0 y), 3 y^2)
@@ -264,7 +269,7 @@ template <bool STY, int NFR>
 __device__ __forceinline__ void tree_store(const FineArgs& a, const double (&S)[2 * NFR], int j, const TreeCtx& c) {
   if constexpr (STY) {
     if (c.t < c.beff) {
-      double* yr = a.Y + y_row(a, c.r0 + c.t + (int64_t)j * a.Mroot) * a.ldy;
+      double* yr = a.Y + (c.ybase + (int64_t)j * c.ystride) * a.ldy;
 #pragma unroll
       for (int cf = 0; cf < NFR; ++cf) {
         const int col = c.c0 + c.cw + cf * 8 + 2 * c.tg;
@@ -548,6 +553,10 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
   }
   c.r0 = bundle * BUN;
   c.beff = (int)((a.Mroot - c.r0) < BUN ? (a.Mroot - c.r0) : BUN);
+  if constexpr (STY) {
+    c.ybase = y_row(a, c.r0 + c.t);
+    c.ystride = y_stride(a);
+  }
   const int64_t rep = blockIdx.y;  // replica (batched randomisation): own X^red, root R and partials
   const double* __restrict__ root = a.root ? a.root + rep * a.rootrep : nullptr;
 

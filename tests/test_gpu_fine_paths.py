@@ -91,6 +91,8 @@ CASES = {
     "gen1_log4": (2, 16, 40, 24, "log4", LAT, INV, "", False, "k_fine<1,BotNone>", 1),
     "gen3_rand": (2, 15, 60, 50, "rand", LAT, INV, "4", False, "k_fine<3,BotNone>", 3),
     "gen2_rand_net": (2, 15, 60, 37, "rand", NET, UNIT, "", False, "k_fine<2,BotNone>", 2),
+    "gen5_chain": (2, 13, 13, 40, "chain", NET, UNIT, "5", False, "k_fine<5,BotNone>", 5),
+    "gen6_chain": (2, 13, 13, 33, "chain", LAT, UNIT, "6", False, "k_fine<6,BotNone>", 6),
     "gen7_chain": (2, 13, 13, 40, "chain", LAT, INV, "7", False, "k_fine<7,BotNone>", 7),
     "gen4_chain_b3": (3, 9, 9, 40, "chain", LAT, INV, "4", False, "k_fine<4,BotNone>", 4),
 }
