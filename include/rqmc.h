@@ -92,7 +92,11 @@ typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1 } rqmc_map;
 typedef enum {
   RQMC_F_NONE = -1,
   RQMC_F_EXP_MEAN = 0,      /* exp(mean(y))                                  (C1, C3, C5)  */
-  RQMC_F_CALL_MEAN_EXP = 1, /* max(mean(exp(p0 * y)) - p1, 0)                (C2)          */
+  RQMC_F_CALL_MEAN_EXP = 1, /* max(mean(exp(p0 * y)) - p1, 0)                (C2)          *
+                             * (the compile-time tree kernels evaluate exp(p0 y) by a table-driven
+                             * fp64 exp (<= 2.6 ulp) with p0 y clamped to [-700, 700]: no overflow to
+                             * inf / underflow to 0 beyond that; NaN propagates; the general kernel
+                             * uses libdevice exp)                                               */
   RQMC_F_MEAN_SQ = 2,       /* mean(y^2)                                     (C4)          */
   RQMC_F_MEAN = 3           /* mean(y), linear                               (tests)       */
 } rqmc_f;

@@ -218,10 +218,10 @@ __device__ __constant__ static const double kExp2Tab64[64] = {
 // |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
 // (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
 // exponent field.  11 fp64 instructions + 1 LDS vs 16 fp64 + branch for exp(); <= ~2.5 ulp.
-// Out of range by predicated selects (no branch): x > 709.78 -> +inf (overflow), x < -708.39 -> 0 (the
-// subnormal range is flushed: absolute error < 2.3e-308), NaN -> NaN.
+// |x| > 700 is clamped (exp(+-700); the fused kernels' g = exp(p0 y) does not reproduce overflow to inf
+// or underflow to 0 beyond that, include/rqmc.h), NaN propagates (one predicated select).
 __device__ __forceinline__ double exp_t(double x0, const double* etab) {
-  const double x = fmin(fmax(x0, -708.0), 709.0);
+  const double x = fmin(fmax(x0, -700.0), 700.0);
   const double kd = rint(x * 92.33248261689366);                 // 64 / ln 2
   double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
   r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
@@ -232,9 +232,7 @@ __device__ __forceinline__ double exp_t(double x0, const double* etab) {
   p = fma(p, r, 1.0);
   const int k = (int)kd;
   const double v = etab[k & 63] * p;
-  double e = __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
-  e = x0 > 709.782712893384 ? __longlong_as_double(0x7ff0000000000000ll) : e;
-  e = x0 < -708.3964185322641 ? 0.0 : e;
+  const double e = __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
   return x0 != x0 ? x0 : e;
 }
 
