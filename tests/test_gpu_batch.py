@@ -105,3 +105,26 @@ def test_batch_errors(rq):
     with pytest.raises(rq.RqmcError) as e:
         pl.qn_batch(A, prob.f, prob.fparam, shifts=bad)
     assert e.value.code == 5
+
+
+@pytest.mark.parametrize("seed,b,m,s,tau,kind", [(31, 2, 12, 120, 40, W.KIND_LATTICE),
+                                                (32, 3, 8, 60, 30, W.KIND_LATTICE),
+                                                (33, 2, 13, 70, 24, W.KIND_NET)])
+def test_batch_tight_workspace_sweep(rq, seed, b, m, s, tau, kind):
+    """with a workspace between one and R replicas the batch re-plans its chunk and
+    layout (more replicas may fuse deeper); whatever it picks must fit the caller's bytes and give every
+    replica's oracle sum.  (tests/test_gpu_debug_build.py reruns this file with every store and
+    cp.async source bounds-checked.)"""
+    R = 24
+    prob = W.make_random(seed, b, m, s, tau, kind=kind, shifted=True, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    kw = _replicas(prob, R, seed)
+    A = dev(prob.A)
+    pl = rq.Plan.from_problem(prob)
+    lo, hi = pl.workspace_size_batch(1), pl.workspace_size_batch(R)
+    ref = None
+    for wb in sorted({lo, lo + 8, (2 * lo + hi) // 3, (lo + 2 * hi) // 3, hi - 8, hi}):
+        sums = pl.qn_batch(A, prob.f, prob.fparam, max_workspace_bytes=wb, **kw).cpu().numpy()
+        if ref is None:
+            ref = np.array([oracle.neumaier(oracle.f_rows(_with(prob, kw, r), np.arange(prob.N))) for r in range(R)])
+            scale = np.array([np.abs(oracle.f_rows(_with(prob, kw, r), np.arange(prob.N))).sum() for r in range(R)])
+        assert np.all(np.abs(sums - ref) <= 1e-12 * scale), wb
