@@ -74,7 +74,11 @@ struct Tree {
   static constexpr int RWN = BUN / 8;                              // row warps (8 residues each)
   static constexpr int NGRP = B;                                   // warp groups: one per top-level run
   static constexpr int WARPS = NGRP * CH * RWN;
+#ifdef RQMC_TREE_MINB
+  static constexpr int MINB = RQMC_TREE_MINB;                      // A/B experiments: CTAs per SM
+#else
   static constexpr int MINB = (8 + WARPS - 1) / WARPS;             // CTAs per SM for >= 8 warps
+#endif
   static constexpr int XP = BUN == 8 ? 12 : (BUN == 16 ? 20 : kPad);  // X^red t-stride (conflict-free)
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int NV = 2 * NFR;                               // doubles per lane per node
