@@ -36,7 +36,11 @@
 
 namespace rqmc {
 
-constexpr int kFftThreads = 256;
+#ifndef RQMC_FFT_CT          // columns per CTA of the pass-1/3 and short-valuation kernels (pass 2: half,
+#define RQMC_FFT_CT 16       // two sequences); 16 workers per column and sequence (8 measured 2 % slower)
+#endif
+constexpr int kFftCT = RQMC_FFT_CT;
+constexpr int kFftThreads = 16 * kFftCT;
 constexpr int kFftSmallLg = 8;     // valuations with L <= 2^8 run in k_fft_small
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -245,9 +249,9 @@ __device__ __forceinline__ void fft_scatter(const FftArgs& a, int vi, const FftV
 
 // pass 1 (valuations [vlo, vhi)): (mode 0) a_v for e = e1 L2 + e2, e1 < L1; (mode 1) H_v; FFT over e1;
 // times w_L^(e2 f1); stored at row f1 L2 + e2
-__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass1(const FftArgs a, int mode, int vlo, int vhi) {
+__global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass1(const FftArgs a, int mode, int vlo, int vhi) {
   pdl_enter();
-  constexpr int CT = 16;
+  constexpr int CT = kFftCT;
   int vi, e2;
   if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
   const FftV V = a.v[vi];
@@ -284,9 +288,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass1(const FftArgs a, i
 // pass 2 (valuations [vlo, vhi), L2 >= 2) on the rows f1 and f1b = -f1 (mod L1): forward FFT over e2;
 // (mode 0) unpack, multiply with H's spectrum, repack, inverse FFT, times conj(w_L^(e2 f1));
 // (mode 1) store the forward spectrum (H)
-__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass2(const FftArgs a, int mode, int vlo, int vhi) {
+__global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass2(const FftArgs a, int mode, int vlo, int vhi) {
   pdl_enter();
-  constexpr int CT = 8;
+  constexpr int CT = kFftCT / 2;
   int vi, f1;
   if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L1 / 2 + 1; }, &vi, &f1)) return;
   const FftV V = a.v[vi];
@@ -346,9 +350,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass2(const FftArgs a, i
 
 // pass 3 (valuations [vlo, vhi)): inverse FFT over f1 -> e1, 1/L, scatter of P^+ (Re) and P^- (Im)
 // at e = e1 L2 + e2
-__global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass3(const FftArgs a, int vlo, int vhi) {
+__global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass3(const FftArgs a, int vlo, int vhi) {
   pdl_enter();
-  constexpr int CT = 16;
+  constexpr int CT = kFftCT;
   int vi, e2;
   if (!fft_task(a, vlo, vhi, blockIdx.y, [](const FftV& V) { return V.L2; }, &vi, &e2)) return;
   const FftV V = a.v[vi];
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_pass3(const FftArgs a, i
 // scatter, and fold a_(v+1)(e) = a_v(e) + a_v(e + L/2) for the next (coarser) valuation
 __global__ void __launch_bounds__(kFftThreads, 1) k_fft_small(const FftArgs a, int vlo) {
   pdl_enter();
-  constexpr int CT = 16;
+  constexpr int CT = kFftCT;
   const FftV V0 = a.v[vlo];
   const int Ls = V0.L, c0 = blockIdx.x * CT;
   extern __shared__ __align__(16) double2 fbuf[];
@@ -469,9 +473,9 @@ cudaError_t launch_fft_level(const FftArgs& a0, cudaStream_t st) {
     else Ls = max(Ls, a0.v[i].L);
   }
   for (int i = vs; i < a0.nv; ++i) L1 = max(L1, a0.v[i].L1);   // pass 1 (mode 1) covers every valuation
-  const int s1 = (int)sizeof(double2) * (L1 * 16 + 2 * L1) + 4 * L1 * (int)sizeof(int);
-  const int s2 = (int)sizeof(double2) * (2 * L2 * 8 + 3 * L2);
-  const int ss = (int)sizeof(double2) * (2 * Ls * 16 + 2 * Ls) + 4 * Ls * (int)sizeof(int);
+  const int s1 = (int)sizeof(double2) * (L1 * kFftCT + 2 * L1) + 4 * L1 * (int)sizeof(int);
+  const int s2 = (int)sizeof(double2) * (2 * L2 * (kFftCT / 2) + 3 * L2);
+  const int ss = (int)sizeof(double2) * (2 * Ls * kFftCT + 2 * Ls) + 4 * Ls * (int)sizeof(int);
   cudaError_t e;
   if ((e = set_smem_once(k_fft_pass1, s1)) != cudaSuccess) return e;
   if ((e = set_smem_once(k_fft_pass2, s2)) != cudaSuccess) return e;
@@ -484,7 +488,8 @@ cudaError_t launch_fft_level(const FftArgs& a0, cudaStream_t st) {
   if ((e = launch_k(k_fft_pass1, dim3(1, n1h), dim3(kFftThreads), s1, st, true, h, 1, 0, h.nv)) != cudaSuccess) return e;
   if (vs > 0 && (e = launch_k(k_fft_pass2, dim3(1, n2), dim3(kFftThreads), s2, st, true, h, 1, 0, vs)) != cudaSuccess)
     return e;
-  const unsigned g16 = (unsigned)((a0.ncol + 15) / 16), g8 = (unsigned)((a0.ncol + 7) / 8);
+  const unsigned g16 = (unsigned)((a0.ncol + kFftCT - 1) / kFftCT);
+  const unsigned g8 = (unsigned)((a0.ncol + kFftCT / 2 - 1) / (kFftCT / 2));
   if (vs > 0) {
     if ((e = launch_k(k_fft_pass1, dim3(g16, n1), dim3(kFftThreads), s1, st, true, a0, 0, 0, vs)) != cudaSuccess) return e;
     if ((e = launch_k(k_fft_pass2, dim3(g8, n2), dim3(kFftThreads), s2, st, true, a0, 0, 0, vs)) != cudaSuccess) return e;
