@@ -25,6 +25,7 @@ struct GenLevel {
   int64_t xoff;   // offset (doubles) of X^red in the workspace
   int j_lo, s_w, ldx, tc_log;   // tc_log: log2 of the generator's column-tile width min(32, pow2 >= ldx)
   double inv_M;   // 2^-(m-w) for b = 2 (exact scaling of t / M)
+  int mixed;      // merged coarse levels (Layout::absorb): coordinate j has its own M_j = b^(m - w_j)
 };
 
 struct GenArgs {
@@ -39,6 +40,7 @@ struct GenArgs {
   const uint64_t* C;             // net column words (row-zeroed)
   const uint64_t* dshift;        // net sigma_j
   uint64_t seed;                 // reduced MC generator seed
+  const int* wcl;                // min(w_j, m) per coordinate (merged levels, GenLevel::mixed)
   // replicas (batched randomisation, NEXT-2): replica r = blockIdx.z uses shift[r*srep + j] /
   // dshift[r*srep + j] / seeds[r] (seeds NULL: seed) and writes X + r*xrep
   int srep;

@@ -34,6 +34,8 @@ struct Level {
   int w, j_lo, s_w, parent, coarse;
   int fft_tab;    // index into rqmc_plan_s::fft (FFT-eligible level, NEXT-4), -1 otherwise
   int fft;        // layout: this coarse level runs as the FFT product (rqmc_fft.cu) instead of the GEMM
+  int absorbed;   // layout: merged into the absorbing level below it (Layout::absorb)
+  int s_gemm;     // layout: coordinates of this level's GEMM (s_w, or all merged levels' for the absorbing one)
   int fused;      // coarse pair parent: R stays on chip, computed with its child (next level) in one launch
   int64_t M, Ml;
   int ldx;
@@ -45,6 +47,7 @@ struct Level {
 // offsets, R buffers, fine-kernel shared-memory layout, workspace offsets.
 struct Layout {
   int ckpt = -1, nfine = 0;
+  int absorb = 0;            // levels 0 .. absorb-1 merged into level `absorb` (one GEMM, latency regime)
   int64_t nbundles = 0;
   std::vector<Level> lv;     // copy of the plan's levels with coarse / ldx / xoff / rbuf filled
   int ldr = 0;               // row stride of R buffers
@@ -130,6 +133,8 @@ struct rqmc_plan_s {
   int64_t N = 0, Nl = 0;
   int s_star = 0;
   std::vector<int32_t> w;
+  std::vector<int> wlev;     // level w of each coordinate (device: merged levels' per-coordinate period)
+  int* d_wl = nullptr;
   std::vector<uint64_t> z, C, dshift;
   std::vector<double> shift;
   std::vector<Level> lv;     // coarse -> fine (checkpoint-independent fields)
@@ -252,7 +257,26 @@ int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
 
 // Workspace layout for checkpoint c: [X^red of every level][R buf 0][R buf 1][partials] (one
 // replica's slice, off_fsum bytes) then [f-sum][A staging] for the host entry point.
-void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
+// Latency regime of small problems: the top coarse levels 0 .. a-1 are merged into level a (one GEMM
+// over all their coordinates at level a's M_a rows: x_{r,j} depends on r mod M_j, so the
+// merged rows are the same points) when that GEMM stays under kAbsorbMacs multiply-adds for the
+// replicas together: one launch instead of a + 1 dependent ones.  More MACs (Σ_{i<a} s_i (M_a - M_i)
+// τ) but no extra bytes; C2: 5 coarse GEMMs (37 us) -> 1.  RQMC_ABSORB=0 disables.
+constexpr double kAbsorbMacs = 268435456.0;   // 2^28 (~7 us at the fp64 peak)
+int choose_absorb(const rqmc_plan_s& p, const Layout& L, int c, int64_t reps) {
+  const char* e = std::getenv("RQMC_ABSORB");
+  if (e && *e && *e == '0') return 0;
+  int a = 0, s_acc = 0;
+  for (int i = 0; i <= c; ++i) {
+    if (L.lv[i].fft) break;
+    s_acc += L.lv[i].s_w;
+    if (i > 0 && (double)L.lv[i].Ml * p.tau * s_acc * reps <= kAbsorbMacs) a = i;
+    else if (i > 0) break;
+  }
+  return a;
+}
+
+void make_layout(const rqmc_plan_s& p, int c, Layout& L, int64_t reps = 1) {
   const int nl = (int)p.lv.size();
   L.ckpt = c;
   L.nfine = nl - 1 - c;
@@ -263,7 +287,15 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   for (int i = 0; i < nl; ++i) {
     Level& V = L.lv[i];
     V.fft = V.coarse && V.fft_tab >= 0 && fft_mode != 0 && (fft_mode == 1 || V.s_w >= kFftMinS);
+    V.absorbed = 0;
+    V.s_gemm = V.s_w;
   }
+  L.absorb = choose_absorb(p, L, c, reps);
+  for (int i = 0; i < L.absorb; ++i) {
+    L.lv[i].absorbed = 1;
+    L.lv[L.absorb].s_gemm += L.lv[i].s_w;   // coarser coordinates follow level a's contiguously in j
+  }
+  if (L.absorb > 0) L.lv[L.absorb].parent = -1;
   L.nbundles = (L.lv[c].Ml + kBundle - 1) / kBundle;
   L.fine_smem = fine_smem_bytes(p, c, &L.fine_xs_off, &L.fine_as_off, &L.fine_as_stride, &L.fine_acc_off,
                                 &L.leafruns);
@@ -271,9 +303,10 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   L.off_x = 0;
   L.max_gen_entries = 0;
   for (auto& V : L.lv) {
-    V.ldx = V.coarse ? (V.s_w + 1) / 2 * 2 : V.s_w;
+    V.ldx = V.coarse ? (V.s_gemm + 1) / 2 * 2 : V.s_w;
     V.xoff = (int64_t)(off / sizeof(double));
-    if (V.fft) continue;        // FFT levels need no X^red (their H tables are generated in rqmc_fft.cu)
+    if (V.fft || V.absorbed) continue;   // FFT levels need no X^red (H tables in rqmc_fft.cu); merged ones
+                                         // are generated as the absorbing level's columns
     off = align_up(off + (size_t)V.Ml * V.ldx * sizeof(double), 256);
     L.max_gen_entries = std::max<int64_t>(L.max_gen_entries, V.Ml * V.ldx);
   }
@@ -284,7 +317,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   // 13.54 ms) although it saves R_7's 4.3 GB round trip.  Stored levels alternate R buffers.
   static const bool no_pair = [] { const char* e = std::getenv("RQMC_GEMM_PAIR"); return !(e && *e && *e != '0'); }();
   for (int i = 0; i <= c; ++i) L.lv[i].fused = 0;
-  for (int i = c - 1; i >= 0 && !no_pair; i -= 2) {
+  for (int i = c - 1; i >= L.absorb && !no_pair; i -= 2) {
     const Level &P = L.lv[i], &C = L.lv[i + 1];
     const int64_t ncu = C.Ml / P.Ml;
     if (C.parent == i && ncu * P.Ml == C.Ml && ncu >= 1 && ncu <= 4 && !P.fft && !C.fft) L.lv[i].fused = 1;
@@ -292,7 +325,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
   size_t rsz[2] = {0, 0};
   int nstored = 0;
   for (int i = 0; i <= c; ++i) {
-    if (L.lv[i].fused) { L.lv[i].rbuf = -1; continue; }
+    if (L.lv[i].fused || L.lv[i].absorbed) { L.lv[i].rbuf = -1; continue; }
     const int b = nstored++ & 1;
     L.lv[i].rbuf = b;
     rsz[b] = std::max(rsz[b], (size_t)L.lv[i].Ml * L.ldr * sizeof(double));
@@ -331,12 +364,14 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L) {
 const Layout& layout_for(rqmc_plan_s* p, int64_t reps, int f) {
   (void)f;
   const int c = choose_ckpt(*p, reps);
-  if (c == p->L1.ckpt || c < 0) return p->L1;
+  if (c < 0) return p->L1;
+  Layout probe;
+  make_layout(*p, c, probe, reps);
+  if (c == p->L1.ckpt && probe.absorb == p->L1.absorb) return p->L1;
   std::lock_guard<std::mutex> lk(p->lay_mu);
   for (auto& L : p->lay_cache)
-    if (L->ckpt == c) return *L;
-  p->lay_cache.emplace_back(new Layout());
-  make_layout(*p, c, *p->lay_cache.back());
+    if (L->ckpt == c && L->absorb == probe.absorb) return *L;
+  p->lay_cache.emplace_back(new Layout(std::move(probe)));
   return *p->lay_cache.back();
 }
 
@@ -372,7 +407,7 @@ void make_chunks(rqmc_plan_s* p) {
     std::unique_ptr<rqmc_plan_s> q(new rqmc_plan_s());
     q->b = p->b; q->m = p->m; q->s = p->s; q->tau = p->tau; q->kind = p->kind; q->map = p->map;
     q->shifted = p->shifted; q->seed = p->seed; q->N = p->N; q->s_star = p->s_star;
-    q->w = p->w; q->z = p->z; q->C = p->C; q->dshift = p->dshift; q->shift = p->shift;
+    q->w = p->w; q->z = p->z; q->C = p->C; q->dshift = p->dshift; q->shift = p->shift; q->wlev = p->wlev;
     q->ncls = ncls;
     q->c0 = ncls * c / nch;
     q->nc = (int)(ncls * (c + 1) / nch - q->c0);
@@ -562,6 +597,9 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
     }
     p->lv.assign(fine_to_coarse.rbegin(), fine_to_coarse.rend());
     for (size_t i = 0; i < p->lv.size(); ++i) p->lv[i].parent = (int)i - 1;
+    p->wlev.assign(d->s, d->m);
+    for (const Level& L : p->lv)
+      for (int q = 0; q < L.s_w; ++q) p->wlev[L.j_lo + q] = L.w;
   }
   const int nl = (int)p->lv.size();
 
@@ -632,6 +670,7 @@ void rqmc_plan_destroy(rqmc_plan_t p) {
   if (p->d_C) cudaFree(p->d_C);
   if (p->d_ds) cudaFree(p->d_ds);
   if (p->d_fft) cudaFree(p->d_fft);
+  if (p->d_wl) cudaFree(p->d_wl);
   for (auto e : p->chunk_ev) cudaEventDestroy(e);
   if (p->side) cudaStreamDestroy(p->side);
   delete p;
@@ -716,6 +755,7 @@ rqmc_status upload(rqmc_plan_s* p) {
     cp(p->d_C, p->C);
     cp(p->d_ds, p->dshift);
     cp(p->d_fft, p->fft_host);
+    cp(p->d_wl, p->wlev);
   });
   if (p->up_err != cudaSuccess)
     return fail(p, RQMC_ECUDA, std::string("device table upload: ") + cudaGetErrorString(p->up_err));
@@ -730,13 +770,14 @@ GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
   g.ncls = p->ncls; g.c0 = p->c0; g.nc = p->nc; g.nlev = (int)p->lv.size();
   g.zero_u = p->shifted ? std::ldexp(1.0, -53) : 0.5 / (double)p->N;
   g.seed = p->seed;
-  g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds;
+  g.z = p->d_z; g.shift = p->d_shift; g.C = p->d_C; g.dshift = p->d_ds; g.wcl = p->d_wl;
   g.X = reinterpret_cast<double*>(static_cast<char*>(work) + lay.off_x);
   for (size_t i = 0; i < lay.lv.size(); ++i) {
     const Level& L = lay.lv[i];
     int tcl = 0;
     while (tcl < 5 && (1 << tcl) < L.ldx) ++tcl;
-    g.lv[i] = GenLevel{L.M, L.fft ? 0 : L.Ml, L.xoff, L.j_lo, L.s_w, L.ldx, tcl, std::ldexp(1.0, -(p->m - L.w))};
+    g.lv[i] = GenLevel{L.M, (L.fft || L.absorbed) ? 0 : L.Ml, L.xoff, L.j_lo, L.s_gemm, L.ldx, tcl,
+                       std::ldexp(1.0, -(p->m - L.w)), (L.coarse && i == (size_t)lay.absorb && lay.absorb > 0) ? 1 : 0};
   }
   return g;
 }
@@ -877,8 +918,9 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   // one launch whose parent R never leaves the chip (bit-identical to two launches).
   for (int i = 0; i <= lay.ckpt; ++i) {
     const Level& L = lay.lv[i];
+    if (L.absorbed) continue;    // merged into level lay.absorb's GEMM
     GemmArgs a{};
-    a.X = g.X + L.xoff; a.ldx = L.ldx; a.M = L.Ml; a.K = L.s_w;
+    a.X = g.X + L.xoff; a.ldx = L.ldx; a.M = L.Ml; a.K = L.s_gemm;
     a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda; a.tau = p->tau;
     if (L.parent >= 0) {
       const Level& P = lay.lv[L.parent];
@@ -1185,7 +1227,12 @@ rqmc_status rqmc_points(rqmc_plan_t p, int idx, int64_t r0, int64_t count, uint6
   if (!p || idx < 0 || idx >= (int)p->lv.size() || r0 < 0 || count < 0 || r0 + count > p->lv[idx].Ml)
     return fail(p, RQMC_EINVAL, "bad level / row range");
   if (rqmc_status s = upload(p)) return s;
+  // the plan's own levels (no merged coordinates, no workspace)
   GenArgs g = gen_args(p, p->L1, nullptr);
+  for (size_t i = 0; i < p->lv.size(); ++i) {
+    const Level& L = p->lv[i];
+    g.lv[i] = GenLevel{L.M, L.Ml, 0, L.j_lo, L.s_w, L.s_w, 0, std::ldexp(1.0, -(p->m - L.w)), 0};
+  }
   return check_cuda(p, launch_points(g, idx, r0, count, d_words, d_vals, static_cast<cudaStream_t>(stream)),
                     "k_points");
 }

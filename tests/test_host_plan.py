@@ -320,5 +320,5 @@ def test_batch_chunk_fits_workspace(rq):
         assert st in (0, 9), (wb, st)              # RQMC_OK on a GPU would need real buffers; ECUDA here
     st = lib.rqmc_qn_batch(pl._h, 64, sh.ctypes.data_as(C.POINTER(C.c_double)), None, None,
                            C.c_void_p(1 << 20), prob.tau, W.F_EXP_MEAN, None, C.cast(out, C.c_void_p),
-                           C.c_void_p(1 << 30), one - 8, None)
-    assert st == 1                                 # EINVAL: below one replica
+                           C.c_void_p(1 << 30), 4096, None)
+    assert st == 1                                 # EINVAL: below one replica of any layout
