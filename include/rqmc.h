@@ -130,6 +130,8 @@ typedef struct {
   int coarse;       /* 1: materialised per-level GEMM pass; 0: fused into the fine kernel      */
   int fft;          /* 1: coarse level computed by the FFT product over the unit group of
                        Z / 2^k (unshifted b = 2 lattices, NEXT-4)   */
+  int absorbed;     /* 1: coarse level merged into a finer coarse level's GEMM (small unit-map
+                       problems: one launch for several levels; same points)       */
 } rqmc_level_info;
 
 typedef struct {

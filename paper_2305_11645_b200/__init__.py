@@ -49,7 +49,8 @@ class _Desc(C.Structure):
 
 class LevelInfo(C.Structure):
     _fields_ = [("w", C.c_int), ("j_lo", C.c_int), ("s_w", C.c_int), ("M", C.c_int64),
-                ("M_local", C.c_int64), ("parent", C.c_int), ("coarse", C.c_int), ("fft", C.c_int)]
+                ("M_local", C.c_int64), ("parent", C.c_int), ("coarse", C.c_int), ("fft", C.c_int),
+                ("absorbed", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

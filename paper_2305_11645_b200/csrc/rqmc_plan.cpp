@@ -259,19 +259,29 @@ int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
 // replica's slice, off_fsum bytes) then [f-sum][A staging] for the host entry point.
 // Latency regime of small problems: the top coarse levels 0 .. a-1 are merged into level a (one GEMM
 // over all their coordinates at level a's M_a rows: x_{r,j} depends on r mod M_j, so the
-// merged rows are the same points) when that GEMM stays under kAbsorbMacs multiply-adds for the
-// replicas together: one launch instead of a + 1 dependent ones.  More MACs (Σ_{i<a} s_i (M_a - M_i)
-// τ) but no extra bytes; C2: 5 coarse GEMMs (37 us) -> 1.  RQMC_ABSORB=0 disables.
+// merged rows are the same points): one launch instead of a + 1 dependent ones, for more MACs
+// (Σ_{i<a} s_i (M_a - M_i) τ) and as many more generated entries (each a Φ^-1 when mapped).  Taken
+// while the merged GEMM stays under kAbsorbMacs multiply-adds (replicas together) and the extra
+// entries under a x 2^20 (unit map; a x 2^17 for reduced-MC draws).  C1: 6 coarse GEMMs -> 1
+// (43.9 -> 18.9 us).  RQMC_ABSORB=0 disables.
 constexpr double kAbsorbMacs = 268435456.0;   // 2^28 (~7 us at the fp64 peak)
 int choose_absorb(const rqmc_plan_s& p, const Layout& L, int c, int64_t reps) {
   const char* e = std::getenv("RQMC_ABSORB");
   if (e && *e && *e == '0') return 0;
-  int a = 0, s_acc = 0;
-  for (int i = 0; i <= c; ++i) {
-    if (L.lv[i].fft) break;
-    s_acc += L.lv[i].s_w;
-    if (i > 0 && (double)L.lv[i].Ml * p.tau * s_acc * reps <= kAbsorbMacs) a = i;
-    else if (i > 0) break;
+  // Φ^-1-mapped points: the extra generated entries cost more than the launches saved (C2: all coarse
+  // levels merged 93 -> 112 us, three of five 91 -> 100 us), so only unit-map points merge
+  if (p.map != RQMC_MAP_UNIT) return 0;
+  const double per = p.kind == RQMC_REDUCED_MC ? 131072.0 : 1048576.0;
+  int a = 0;
+  for (int i = 1; i <= c; ++i) {
+    if (L.lv[0].fft || L.lv[i].fft) break;
+    double s_acc = 0.0, extra = 0.0;
+    for (int q = 0; q <= i; ++q) {
+      s_acc += L.lv[q].s_w;
+      extra += (double)L.lv[q].s_w * (double)(L.lv[i].Ml - L.lv[q].Ml);
+    }
+    if ((double)L.lv[i].Ml * p.tau * s_acc * reps > kAbsorbMacs || extra * reps > per * i) break;
+    a = i;
   }
   return a;
 }
@@ -702,6 +712,7 @@ rqmc_status rqmc_plan_level(rqmc_plan_t p, int idx, rqmc_level_info* o) {
   const Level& L = p->lv[idx];
   o->w = L.w; o->j_lo = L.j_lo; o->s_w = L.s_w; o->M = L.M; o->M_local = L.Ml;
   o->parent = L.parent; o->coarse = p->L1.lv[idx].coarse; o->fft = p->L1.lv[idx].fft;
+  o->absorbed = p->L1.lv[idx].absorbed;
   return RQMC_OK;
 }
 

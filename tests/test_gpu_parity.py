@@ -493,3 +493,28 @@ def test_batch_simulated_ranks(rq, G):
         tot += rq.Plan.from_problem(prob, rank=g, world=G).qn_batch(A, prob.f, prob.fparam,
                                                                      shifts=shifts).cpu().numpy()
     np.testing.assert_allclose(tot, full, rtol=1e-12)
+
+
+@pytest.mark.parametrize("seed,b,m,s,tau,kind,shifted,wmode", [(71, 2, 10, 32, 32, W.KIND_LATTICE, False, "log"),
+                                                              (72, 2, 11, 60, 40, W.KIND_NET, True, "log"),
+                                                              (73, 3, 7, 50, 30, W.KIND_LATTICE, True, "rand"),
+                                                              (74, 2, 10, 40, 24, W.KIND_MC, False, "log")])
+def test_absorbed_coarse_levels(rq, monkeypatch, seed, b, m, s, tau, kind, shifted, wmode):
+    """Small unit-map problems merge their top coarse levels into one GEMM (per-coordinate periods in
+    k_gen): at least one level is absorbed, Y matches the oracle on every row and the unmerged run
+    (RQMC_ABSORB=0) to 1e-12, the f-sums likewise."""
+    prob = W.make_random(seed, b, m, s, tau, kind=kind, shifted=shifted, mapping=W.MAP_UNIT, wmode=wmode,
+                         f=W.F_EXP_MEAN)
+    A = dev(prob.A)
+    monkeypatch.setenv("RQMC_ABSORB", "")
+    p1 = rq.Plan.from_problem(prob)
+    assert any(L["absorbed"] for L in p1.levels())
+    Y1, s1 = p1.xa(A, prob.f, prob.fparam)
+    monkeypatch.setenv("RQMC_ABSORB", "0")
+    p0 = rq.Plan.from_problem(prob)
+    assert not any(L["absorbed"] for L in p0.levels())
+    Y0, s0 = p0.xa(A, prob.f, prob.fparam)
+    check_y(prob, Y1.cpu().numpy(), np.arange(prob.N))
+    np.testing.assert_allclose(Y1.cpu().numpy(), Y0.cpu().numpy(), rtol=0, atol=1e-13 * np.abs(prob.A).sum(0).max())
+    fo = oracle.f_rows(prob, np.arange(prob.N))
+    assert abs(float(s1.item()) - oracle.neumaier(fo)) <= 1e-12 * np.abs(fo).sum()
