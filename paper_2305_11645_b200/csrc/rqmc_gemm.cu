@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(BM / (8 * WMF) * 32 * kGemmWN) k_level_gemm(co
 // X^red tile (64 rows x 16 k) and the A tile (16 k x 64 columns, four 16 x 16 boxes) of each k-tile are
 // brought in by cp.async.bulk.tensor with 128-byte swizzle, completing on one mbarrier per stage
 // (3-stage ring, thread 0 issues); the 4 warps read the DMMA fragments through the swizzle.  Same
-// arithmetic and k order as k_level_gemm (bit-identical R).  Single replica, K % 16 == 0, 16-byte
-// aligned A / lda even, 64-row slices.
+// arithmetic and k order as k_level_gemm (bit-identical R; a ragged last k-tile multiplies the
+// zero fill).  Single replica, 16-byte aligned A / lda even, 64-row slices.
 // ------------------------------------------------------------------------------------------
 constexpr int kTmaStages = 3;
 constexpr int kTmaStageBytes = 64 * 16 * 8 + 4 * 16 * 16 * 8;   // X tile + 4 A boxes = 16 KB
@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(128) k_level_gemm_tma(const GemmArgs a, const 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int nk = a.K / BK;
+  const int nk = (a.K + BK - 1) / BK;   // a ragged last tile: TMA zero-fills rows >= K of A and
+                                        // columns >= ldx of X^red (k_gen zeroes [s_w, ldx))
   auto issue = [&](int kt) {   // thread 0: stage kt's X tile and A boxes
     unsigned char* sb = base + (kt % NST) * kTmaStageBytes;
     uint64_t* b = &bar[kt % NST];
@@ -416,7 +417,7 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
   // K = 128 level 12.6 us vs ~9 us)
   const int64_t ncta = nrb * ((a.tau + 63) / 64);
   const bool use_tma = tma_mode == 1 || (tma_mode < 0 && a.K >= 128 && ncta >= 592);
-  if (use_tma && BM == 64 && !pair && vec && nrep == 1 && a.K % 16 == 0 && mp_blk % 64 == 0 && a.ldx % 2 == 0 &&
+  if (use_tma && BM == 64 && !pair && vec && nrep == 1 && mp_blk % 64 == 0 && a.ldx % 2 == 0 &&
       a.M < (int64_t(1) << 31) &&
       (uintptr_t)a.X % 16 == 0) {
     const cudaError_t e = launch_gemm_tma(a, mp_blk, nu, nrb, st);
