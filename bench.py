@@ -351,8 +351,16 @@ def main():
                  "t_roof_ms": t_roof * 1e3, "achieved_tflops": f_step / t_step / 1e12,
                  "achieved_gbs": b_step / t_step / 1e9, "frac": t_roof / t_step}
 
-    n_coarse = ck + 1
-    launches_per_step = 1 + n_coarse + 1 + 1   # k_gen + coarse GEMMs + k_fine + k_reduce
+    def level_launches(L):       # kernels one coarse level launches (rqmc_plan.cpp run_core)
+        if L["absorbed"]:
+            return 0               # merged into a finer level's GEMM
+        if L["fft"]:               # rqmc_fft.cu launch_fft_level: valuations v < vs use the 3 passes
+            k = prob.m - L["w"]
+            vs = max(0, k - 10)
+            return 1 + (1 if vs else 0) + (3 if vs else 0) + (1 if vs < k - 2 else 0) + 1
+        return 1
+    # k_gen + coarse levels + k_fine + k_reduce (x R / chunk count for batches: one sequence per chunk)
+    launches_per_step = 1 + sum(level_launches(L) for L in levels[:ck + 1]) + 1 + 1
     line = {
         "metric": METRIC,
         "value": R * prob.N * prob.tau / (ms_max / args.steps * 1e-3),

@@ -65,6 +65,7 @@ def lib():
         _lib.orc_alg4_product.argtypes = [C.POINTER(_Prob), dp, C.c_int, dp]
         _lib.orc_mc_bank_index.restype = C.c_uint64
         _lib.orc_mc_bank_index.argtypes = [C.POINTER(_Prob), C.c_uint64, C.c_int]
+        _lib.orc_mc_bank_indices.argtypes = [C.POINTER(_Prob), C.c_uint64, u64p]
         _lib.orc_mc_word.restype = C.c_uint64
         _lib.orc_mc_word.argtypes = [C.c_uint64, C.c_int, C.c_uint64]
         _lib.orc_mc_points_bank.argtypes = [C.POINTER(_Prob), dp, i64p, C.c_int64, C.c_int64, dp]
@@ -94,6 +95,14 @@ def mc_bank_index(prob, n: int, j: int) -> int:
     """Reduced MC (Eq. randpts): bank sample number used by coordinate j (0-based) of point n."""
     h = _Holder(prob)
     return int(lib().orc_mc_bank_index(C.byref(h.s), n, j))
+
+
+def mc_bank_indices(prob, n: int) -> np.ndarray:
+    """Reduced MC (Eq. randpts): the bank sample numbers of every coordinate of point n, one digit pass."""
+    h = _Holder(prob)
+    out = np.empty(prob.s, dtype=np.uint64)
+    lib().orc_mc_bank_indices(C.byref(h.s), n, _ptr(out, C.c_uint64))
+    return out
 
 
 def mc_word(seed: int, j: int, r: int) -> int:

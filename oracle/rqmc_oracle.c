@@ -100,6 +100,21 @@ uint64_t orc_mc_bank_index(const orc_problem* p, uint64_t n, int j) {
   return idx;
 }
 
+/* All coordinates' bank indices of point n in one pass: the digits m_i of Eq. randpts do not depend
+ * on j, so idx[j] = sum_{i >= j} m_i N_{i+1} is a suffix sum (same recurrence as orc_mc_bank_index). */
+void orc_mc_bank_indices(const orc_problem* p, uint64_t n, uint64_t* idx) {
+  uint64_t rem = n, acc = 0;
+  for (int i = p->s - 1; i >= 0; --i) {
+    const int wi = p->w[i] < p->m ? p->w[i] : p->m;
+    const int wn = (i + 1 < p->s) ? (p->w[i + 1] < p->m ? p->w[i + 1] : p->m) : p->m;
+    const uint64_t Ni1 = ipow((uint64_t)p->b, p->m - wn);
+    const uint64_t Mi = ipow((uint64_t)p->b, wn - wi);
+    acc += (rem % Mi) * Ni1;
+    rem /= Mi;
+    idx[i] = acc;
+  }
+}
+
 /* the counter-based draw y_{j,r} (include/rqmc.h, rqmc_kind): 53-bit word and u = (word|1) 2^-53 */
 static uint64_t orc_mix64(uint64_t x) {
   x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
@@ -123,6 +138,14 @@ int orc_mc_points_bank(const orc_problem* p, const double* bank, const int64_t* 
   return 0;
 }
 
+/* reduced MC: coordinate j's draw from bank index idx, mapped */
+static double orc_mc_value(const orc_problem* p, int j, uint64_t idx, uint64_t* word_out) {
+  const uint64_t word = orc_mc_word(p->seed, j, idx);
+  if (word_out) *word_out = word;
+  const double u = (double)(word | 1u) * ldexp(1.0, -53);    /* in (0,1): no zero rule needed */
+  return p->map == 0 ? u : orc_invnorm(u);
+}
+
 /* O1 for one entry: coordinate j of point k (value, and its integer word in *word). */
 double orc_point(const orc_problem* p, uint64_t k, int j, uint64_t* word_out) {
   const uint64_t N = ipow((uint64_t)p->b, p->m);
@@ -130,12 +153,7 @@ double orc_point(const orc_problem* p, uint64_t k, int j, uint64_t* word_out) {
   double u;
   uint64_t word;
   int shifted;
-  if (p->kind == 2) {
-    word = orc_mc_word(p->seed, j, orc_mc_bank_index(p, k, j));
-    if (word_out) *word_out = word;
-    u = (double)(word | 1u) * ldexp(1.0, -53);              /* in (0,1): no zero rule needed */
-    return p->map == 0 ? u : orc_invnorm(u);
-  }
+  if (p->kind == 2) return orc_mc_value(p, j, orc_mc_bank_index(p, k, j), word_out);
   if (p->kind == 0) {
     /* z_j = b^{w_j} z'_j; for w_j >= m, z_j is a multiple of N. */
     uint64_t zj = wj >= p->m ? 0 : (uint64_t)(((unsigned __int128)ipow((uint64_t)p->b, wj) * p->z[j]) % N);
@@ -319,9 +337,26 @@ int orc_f_all_meanid_tab(const orc_problem* p, const double* A, int tau, int f, 
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
+  if (p->kind == 2) {
+    /* reduced MC: entries r < M_j of every column j from one digit pass per r (orc_mc_bank_indices) */
+    uint64_t Mmax = 0;
+    for (int j = 0; j < p->s; ++j) Mmax = M[j] > Mmax ? M[j] : Mmax;
+#pragma omp parallel
+    {
+      uint64_t* idx = (uint64_t*)malloc(sizeof(uint64_t) * p->s);
+#pragma omp for schedule(static, 1024)
+      for (int64_t r = 0; r < (int64_t)Mmax; ++r) {
+        orc_mc_bank_indices(p, (uint64_t)r, idx);
+        for (int j = 0; j < p->s; ++j)
+          if ((uint64_t)r < M[j]) tab[off[j] + r] = orc_mc_value(p, j, idx[j], NULL);
+      }
+      free(idx);
+    }
+  } else {
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int j = 0; j < p->s; ++j)
-    for (uint64_t r = 0; r < M[j]; ++r) tab[off[j] + r] = orc_point(p, r, j, NULL);
+    for (int j = 0; j < p->s; ++j)
+      for (uint64_t r = 0; r < M[j]; ++r) tab[off[j] + r] = orc_point(p, r, j, NULL);
+  }
 #pragma omp parallel for schedule(static, 4096)
   for (int64_t k = 0; k < (int64_t)N; ++k) {
     double acc = 0.0;

@@ -168,3 +168,14 @@ def test_points_follow_bank_draws():
             wd = oracle.mc_word(99, j, r)
             assert int(T[n, j]) == wd
             assert X[n, j] == oracle.invnorm((wd | 1) * 2.0 ** -53)
+
+
+def test_bank_indices_one_pass_equals_per_coordinate():
+    """orc_mc_bank_indices (one digit pass per point, used by the full-N tabulation) equals the
+    per-coordinate Eq. randpts index orc_mc_bank_index for every coordinate (random layouts, w > m)."""
+    rng = np.random.default_rng(17)
+    for b, m in ((2, 9), (3, 6), (5, 4)):
+        prob = W.make_random(60 + b, b, m, 40, 3, kind=W.KIND_MC, wmode="rand")
+        for n in list(rng.integers(0, prob.N, 40)) + [0, prob.N - 1]:
+            got = oracle.mc_bank_indices(prob, int(n))
+            assert [int(v) for v in got] == [oracle.mc_bank_index(prob, int(n), j) for j in range(prob.s)]
