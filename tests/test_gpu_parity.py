@@ -479,7 +479,7 @@ def test_graph_cache_many_keys_and_pageable_host(rq):
     assert h == ref
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 4, 3])
 def test_batch_simulated_ranks(rq, G):
     """Batched shifts under the residue partition: per rank and replica, the partial sums over the
     G ranks add up to the world = 1 batch result."""
@@ -518,3 +518,20 @@ def test_absorbed_coarse_levels(rq, monkeypatch, seed, b, m, s, tau, kind, shift
     np.testing.assert_allclose(Y1.cpu().numpy(), Y0.cpu().numpy(), rtol=0, atol=1e-13 * np.abs(prob.A).sum(0).max())
     fo = oracle.f_rows(prob, np.arange(prob.N))
     assert abs(float(s1.item()) - oracle.neumaier(fo)) <= 1e-12 * np.abs(fo).sum()
+
+
+def test_fft_levels_single_process_only(rq, monkeypatch):
+    """Reading FFT-2: the FFT product computes every row of a level, so multi-rank plans keep the GEMM
+    for those levels; the ranks' sums still add up to the world-1 (FFT) result."""
+    monkeypatch.setenv("RQMC_FFT", "1")
+    prob = W.make_random(88, 2, 13, 120, 48, shifted=False, mapping=W.MAP_INVNORM, f=W.F_EXP_MEAN)
+    A = dev(prob.A)
+    one = rq.Plan.from_problem(prob)
+    assert any(L["fft"] for L in one.levels())
+    ref = float(one.qn_sum(A, prob.f, prob.fparam).item())
+    tot = 0.0
+    for g in range(4):
+        pg = rq.Plan.from_problem(prob, rank=g, world=4)
+        assert not any(L["fft"] for L in pg.levels())
+        tot += float(pg.qn_sum(A, prob.f, prob.fparam).item())
+    assert abs(tot - ref) <= 1e-12 * abs(ref)
