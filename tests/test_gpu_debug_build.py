@@ -24,7 +24,7 @@ def test_parity_subset_under_bounds_checks():
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
            os.path.join(ROOT, "tests", "test_gpu_fine_paths.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py"),
            os.path.join(ROOT, "tests", "test_gpu_batch.py"), os.path.join(ROOT, "tests", "test_gpu_fft.py"),
-           "-k", "not config and not qn_host and not pair_fusion"]
+           "-k", "not config and not qn_host and not pair_fusion and not sweep and not graph and not exact"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "debug_build_run.log"), "w") as fh:
