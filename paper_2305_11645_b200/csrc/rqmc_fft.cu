@@ -107,60 +107,60 @@ __device__ __forceinline__ void dft_reg(double2 (&r)[16], const double2* tw, int
     }
   }
 }
-template <bool INV>
-__device__ __forceinline__ void dft_reg_n(double2 (&r)[16], int lgn, const double2* tw, int ts) {
-  switch (lgn) {
-    case 1: dft_reg<2, INV>(r, tw, ts); break;
-    case 2: dft_reg<4, INV>(r, tw, ts); break;
-    case 3: dft_reg<8, INV>(r, tw, ts); break;
-    case 4: dft_reg<16, INV>(r, tw, ts); break;
-    default: break;
+
+template <int CT, int S, bool INV, int LG>
+__device__ __forceinline__ void fft_smem_t(double2* buf, const double2* tw) {
+  constexpr int QW = kFftThreads / (S * CT);
+  constexpr int n = 1 << LG, L1 = (LG + 1) >> 1, L2 = LG >> 1, n1 = 1 << L1, n2 = 1 << L2;
+  static_assert(n1 <= QW && n2 <= QW, "one sequence position per worker");
+  const int col = threadIdx.x % CT, s = (threadIdx.x / CT) % S, q = threadIdx.x / (CT * S);
+  double2* b = buf + (size_t)s * n * CT + col;
+  if (q < n2) {
+    double2 r[16];
+#pragma unroll
+    for (int i = 0; i < n1; ++i) r[i] = b[(i * n2 + q) * CT];
+    dft_reg<n1, INV>(r, tw, n / n1);
+#pragma unroll
+    for (int i = 0; i < n1; ++i) {
+      double2 w = tw[(q * i) & (n - 1)];
+      if (INV) w.y = -w.y;
+      b[(i * n2 + q) * CT] = cmul(r[i], w);
+    }
+  }
+  __syncthreads();
+  if constexpr (L2 > 0) {
+    double2 r2[16];
+    if (q < n1) {
+#pragma unroll
+      for (int i = 0; i < n2; ++i) r2[i] = b[(q * n2 + i) * CT];
+      dft_reg<n2, INV>(r2, tw, n / n2);
+    }
+    __syncthreads();
+    if (q < n1) {
+#pragma unroll
+      for (int i = 0; i < n2; ++i) b[(q + n1 * i) * CT] = r2[i];
+    }
+    __syncthreads();
   }
 }
 
 // FFT of length n = 2^lg (lg <= 8) along the rows of S sequences x CT columns in shared memory,
-// buf[(s n + row) CT + col], natural order in and out; 256 threads = S x CT x (256 / (S CT)) workers.
+// buf[(s n + row) CT + col], natural order in and out; kFftThreads = S x CT x 16 workers.
 // n = n1 n2 (n1 = 2^ceil(lg/2), n2 = 2^floor(lg/2)): worker q < n2 transforms x[i1 n2 + q] over i1 and
 // applies w_n^(q k1); worker q < n1 then transforms over the n2 rows q n2 + i2 into X[q + n1 k2].
-// tw: w_n^j = tw[j tws], j < n.  inv: conjugate twiddles (unscaled).  Ends with a barrier.
+// tw: w_n^j, j < n.  INV: conjugate twiddles (unscaled).  Compile-time sizes per lg.  Ends with a barrier.
 template <int CT, int S, bool INV>
-__device__ void fft_smem(double2* buf, int lg, const double2* tw, int tws = 1) {
-  constexpr int QW = kFftThreads / (S * CT);
-  const int col = threadIdx.x % CT, s = (threadIdx.x / CT) % S, q = threadIdx.x / (CT * S);
-  const int n = 1 << lg, l1 = (lg + 1) >> 1, l2 = lg >> 1, n1 = 1 << l1, n2 = 1 << l2;
-  double2* b = buf + (size_t)s * n * CT + col;
-  double2 r[16];
-  for (int qq = q; qq < n2; qq += QW) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < n1) r[i] = b[(i * n2 + qq) * CT];
-    dft_reg_n<INV>(r, l1, tw, (n / n1) * tws);
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < n1) {
-        double2 w = tw[((qq * i) & (n - 1)) * tws];
-        if (INV) w.y = -w.y;
-        b[(i * n2 + qq) * CT] = cmul(r[i], w);
-      }
+__device__ __forceinline__ void fft_smem(double2* buf, int lg, const double2* tw) {
+  switch (lg) {
+    case 1: fft_smem_t<CT, S, INV, 1>(buf, tw); break;
+    case 2: fft_smem_t<CT, S, INV, 2>(buf, tw); break;
+    case 3: fft_smem_t<CT, S, INV, 3>(buf, tw); break;
+    case 4: fft_smem_t<CT, S, INV, 4>(buf, tw); break;
+    case 5: fft_smem_t<CT, S, INV, 5>(buf, tw); break;
+    case 6: fft_smem_t<CT, S, INV, 6>(buf, tw); break;
+    case 7: fft_smem_t<CT, S, INV, 7>(buf, tw); break;
+    default: fft_smem_t<CT, S, INV, 8>(buf, tw); break;
   }
-  __syncthreads();
-  if (l2 == 0) return;
-  double2 r2[16];
-  // each worker keeps <= 1 sequence position in registers across the barrier (n1 <= 16 <= QW)
-  const bool act = q < n1;
-  if (act) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < n2) r2[i] = b[(q * n2 + i) * CT];
-    dft_reg_n<INV>(r2, l2, tw, (n / n2) * tws);
-  }
-  __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < n2) b[(q + n1 * i) * CT] = r2[i];
-  }
-  __syncthreads();
 }
 
 // blockIdx.y -> (v, idx) for v in [vlo, vhi) where valuation v owns cnt(v) consecutive indices
@@ -210,13 +210,24 @@ __device__ __forceinline__ void fft_mult(double2 za, double2 zb, double2 ha, dou
   *wa = make_double2(Pp.x - Pm.y, Pp.y + Pm.x);   // P^+(f) + i P^-(f)
   *wb = make_double2(Pp.x + Pm.y, Pm.x - Pp.y);   // conj(P^+(f)) + i conj(P^-(f)) = value at -f
 }
-// R[r, c] = P / L + R_parent[r mod M_parent, c] for the rows r = 2^v (+-5^e mod 2^K) of the n entries
-// buf[t] (e = (t / CT) es + e0, column c0 + t % CT); 4 entries per thread in flight (parent loads)
-template <int CT>
-__device__ __forceinline__ void fft_scatter(const FftArgs& a, int vi, const FftV& V, const double2* buf, int e0,
-                                            int es, int n, int c0) {
+// rows[2 i], rows[2 i + 1] = 2^v (5^e mod 2^K), 2^v (-5^e mod 2^K) for e = i es + e0, i < nr (once per
+// CTA and row: the CT columns of a row share them)
+__device__ __forceinline__ void fft_rows_of(const FftArgs& a, int vi, int e0, int es, int nr, int64_t* rows) {
   const int K = a.k - vi;
   const uint32_t mK = (K >= 32) ? 0xffffffffu : ((1u << K) - 1);
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    const uint32_t w5 = pow5(i * es + e0, K);
+    rows[2 * i] = (int64_t)w5 << vi;
+    rows[2 * i + 1] = (int64_t)((0u - w5) & mK) << vi;
+  }
+}
+
+// R[r, c] = P / L + R_parent[r mod M_parent, c] for the rows r = rows[2 (t / CT)] (P^+) and
+// rows[2 (t / CT) + 1] (P^-) of the n entries buf[t] (column c0 + t % CT); 4 entries per thread in
+// flight (parent loads)
+template <int CT>
+__device__ __forceinline__ void fft_scatter(const FftArgs& a, const FftV& V, const double2* buf, const int64_t* rows,
+                                            int n, int c0) {
   const double sc = 1.0 / (double)V.L;
   for (int t0 = threadIdx.x; t0 < n; t0 += 4 * blockDim.x) {
     int64_t rp[4], rm[4];
@@ -226,9 +237,8 @@ __device__ __forceinline__ void fft_scatter(const FftArgs& a, int vi, const FftV
       const int t = t0 + u * blockDim.x, c = c0 + (t % CT);
       rp[u] = -1;
       if (t < n && c < a.ncol) {
-        const uint32_t w5 = pow5((t / CT) * es + e0, K);
-        rp[u] = (int64_t)w5 << vi;
-        rm[u] = (int64_t)((0u - w5) & mK) << vi;
+        rp[u] = rows[2 * (t / CT)];
+        rm[u] = rows[2 * (t / CT) + 1];
         pp[u] = a.Rp ? a.Rp[(rp[u] % a.Mp) * a.ldp + c] : 0.0;
         pm[u] = a.Rp ? a.Rp[(rm[u] % a.Mp) * a.ldp + c] : 0.0;
       }
@@ -302,6 +312,7 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass2(co
   double2* b1 = b0 + V.L2 * CT;
   double2* tw = b1 + V.L2 * CT;              // L2
   double2* tr = tw + V.L2;                   // 2 L2 row twiddles
+  double2* hs = tr + 2 * V.L2;               // H's spectrum on the rows f1, f1b (2 L2; mode 0)
   fft_twiddles(tw, V.L2);
   for (int e2 = threadIdx.x; e2 < V.L2; e2 += blockDim.x) {
     tr[e2] = cexpi(((int64_t)e2 * f1) & (V.L - 1), V.L);
@@ -314,6 +325,9 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass2(co
     const bool ok = c < a.ncol && (sq == 0 || two);
     cp_async16(b0 + t, ok ? (sq ? z1 : z0) + (int64_t)e2 * a.ldz + c : a.Z, ok);
   }
+  if (mode == 0)   // H's rows f1 and f1b (contiguous in its block) come in with the data
+    for (int t = threadIdx.x; t < 2 * V.L2; t += blockDim.x)
+      cp_async16(hs + t, a.H + V.hoff + (int64_t)((t < V.L2 ? f1 : f1b) * V.L2 + (t % V.L2)), true);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
@@ -327,7 +341,6 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass2(co
   }
   // pairs {f, -f}: f = f1 + L1 f2 in b0[f2]; -f in (two ? b1 : b0)[f2'], f2' = L2-1-f2 (f1 != 0) or
   // (L2 - f2) mod L2 (f1 = 0).  One thread per unordered pair, results written in place.
-  const double2* H = a.H + V.hoff;
   for (int t = threadIdx.x; t < V.L2 * CT; t += blockDim.x) {
     const int f2 = t / CT, col = t % CT;
     const int f2p = f1 != 0 ? V.L2 - 1 - f2 : ((V.L2 - f2) & (V.L2 - 1));
@@ -335,7 +348,7 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass2(co
     double2* pa = b0 + f2 * CT + col;
     double2* pb = (two ? b1 : b0) + f2p * CT + col;
     double2 wa, wb;
-    fft_mult(*pa, *pb, H[f1 * V.L2 + f2], H[f1b * V.L2 + f2p], &wa, &wb);
+    fft_mult(*pa, *pb, hs[f2], hs[V.L2 + f2p], &wa, &wb);
     *pa = wa;
     if (pb != pa) *pb = wb;
   }
@@ -360,7 +373,9 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass3(co
   extern __shared__ __align__(16) double2 fbuf[];
   double2* buf = fbuf;
   double2* tw = buf + V.L1 * CT;
+  int64_t* rows = reinterpret_cast<int64_t*>(tw + V.L1);   // 2 L1 (the pass-1 layout's tr / rng space)
   fft_twiddles(tw, V.L1);
+  fft_rows_of(a, vi, e2, V.L2, V.L1, rows);
   for (int t = threadIdx.x; t < V.L1 * CT; t += blockDim.x) {
     const int f1 = t / CT, c = c0 + (t % CT);
     cp_async16(buf + t, c < a.ncol ? a.Z + V.zoff + (int64_t)(f1 * V.L2 + e2) * a.ldz + c : a.Z, c < a.ncol);
@@ -369,7 +384,7 @@ __global__ void __launch_bounds__(kFftThreads, 512 / kFftThreads) k_fft_pass3(co
   cp_async_wait<0>();
   __syncthreads();
   fft_smem<CT, 1, true>(buf, V.lgL1, tw);
-  fft_scatter<CT>(a, vi, V, buf, e2, V.L2, V.L1 * CT, c0);
+  fft_scatter<CT>(a, V, buf, rows, V.L1 * CT, c0);
 }
 
 // valuations [vlo, nv) with L <= 256 (L2 = 1), all in one CTA per column tile: gather a_vlo, then per
@@ -403,6 +418,8 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft_small(const FftArgs a, i
     for (int j = threadIdx.x; j < V.L; j += blockDim.x) tw[j] = twL[j * tws];
     __syncthreads();
     fft_smem<CT, 1, false>(buf, V.p, tw);
+    int64_t* rows = reinterpret_cast<int64_t*>(rng);            // the gather bounds are dead by now
+    fft_rows_of(a, vi, 0, 1, V.L, rows);
     const double2* H = a.H + V.hoff;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       const int f = t / CT, col = t % CT, fb = (V.L - f) & (V.L - 1);
@@ -414,7 +431,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft_small(const FftArgs a, i
     }
     __syncthreads();
     fft_smem<CT, 1, true>(buf, V.p, tw);
-    fft_scatter<CT>(a, vi, V, buf, 0, 1, n, c0);
+    fft_scatter<CT>(a, V, buf, rows, n, c0);
     for (int t = threadIdx.x; t < n / 2; t += blockDim.x) acc[t] = cadd(acc[t], acc[t + n / 2]);
     __syncthreads();
   }
@@ -474,7 +491,7 @@ cudaError_t launch_fft_level(const FftArgs& a0, cudaStream_t st) {
   }
   for (int i = vs; i < a0.nv; ++i) L1 = max(L1, a0.v[i].L1);   // pass 1 (mode 1) covers every valuation
   const int s1 = (int)sizeof(double2) * (L1 * kFftCT + 2 * L1) + 4 * L1 * (int)sizeof(int);
-  const int s2 = (int)sizeof(double2) * (2 * L2 * (kFftCT / 2) + 3 * L2);
+  const int s2 = (int)sizeof(double2) * (2 * L2 * (kFftCT / 2) + 5 * L2);
   const int ss = (int)sizeof(double2) * (2 * Ls * kFftCT + 2 * Ls) + 4 * Ls * (int)sizeof(int);
   cudaError_t e;
   if ((e = set_smem_once(k_fft_pass1, s1)) != cudaSuccess) return e;

@@ -117,11 +117,11 @@ uint32_t dlog5(uint64_t z, int k) {
 // level), 3 <= k = m - w <= 18 (FFT lengths L = 2^(k-2-v) <= 2^16 = 256 x 256, two passes)
 constexpr int kFftMinK = 3, kFftMaxK = 18;
 // default rule: the FFT replaces s_w M tau MACs by ~5 M log2 M tau flops plus three passes over its
-// scratch (HBM-bound, measured 24-65 ps per R element on C5U: profiles/r02_fft_levels_C5U.txt) while
-// the DMMA GEMM costs ~60 fs per coordinate and element; measured crossover between s_w = 512 and 1024
-// (C5U: w = 11 / 10 FFT 1.1 / 1.6 ms vs GEMM 2.1 ms; w = 9 2.5 vs 2.1 ms).  RQMC_FFT=1 forces every
+// scratch (HBM-bound, 1.2-2.2 TB/s measured) while the DMMA GEMM costs ~60 fs per coordinate and
+// element; measured crossover at s_w = 512 (C5U: w = 11 / 10 / 9 FFT 0.87 / 1.23 / 1.91 ms vs GEMM
+// 2.01-2.03 ms; w = 8 3.18 vs 2.02 ms; profiles/r02_fft_levels_C5U_v2.txt).  RQMC_FFT=1 forces every
 // eligible coarse level, RQMC_FFT=0 disables.
-constexpr int kFftMinS = 1024;
+constexpr int kFftMinS = 512;
 
 }  // namespace
 

@@ -5,7 +5,7 @@ level's product P_w = X^red_w A_w by FFTs over the unit group of Z/2^k (rqmc_fft
 DMMA GEMM.  It reaches the same XA, so the naive oracle is its check: every row of Y within
 1e-12 max(1, |x_k|_inf) |A_c|_1 and Q_N within relative 1e-12, on random level shapes with every
 level forced onto the FFT (RQMC_FFT=1, RQMC_CKPT_W=0 makes every level coarse), on C1 (forced) and
-on the unshifted Phi^-1-mapped C5 shape at full size (default rule: levels with s_w >= 64).
+on the unshifted Phi^-1-mapped C5 shape at full size (default rule: levels with s_w >= 512).
 """
 import numpy as np
 import pytest
@@ -66,7 +66,7 @@ def test_fft_config_c1(rq, monkeypatch, ck):
 
 @pytest.mark.parametrize("force", ["", "1"])
 def test_fft_config_c5u(rq, monkeypatch, force):
-    """Unshifted, Phi^-1-mapped C5 shape (C5U) at full size, with the default rule (levels w = 10, 11 on
+    """Unshifted, Phi^-1-mapped C5 shape (C5U) at full size, with the default rule (levels w = 9-11 on
     the FFT) and with every coarse level (w = 6..12) forced onto it: Q_N over all 2^24 points against
     the oracle's O3' on every row, and sampled rows of a 64-column panel of Y against the naive
     oracle."""
@@ -74,8 +74,8 @@ def test_fft_config_c5u(rq, monkeypatch, force):
     prob = W.make_config("C5U")
     pl = rq.Plan.from_problem(prob)
     lv = pl.levels()
-    exp = [11, 10] if not force else [12, 11, 10, 9, 8, 7, 6]
-    assert [L["w"] for L in lv if L["fft"]] == exp                # default rule: s_w >= 1024
+    exp = [11, 10, 9] if not force else [12, 11, 10, 9, 8, 7, 6]
+    assert [L["w"] for L in lv if L["fft"]] == exp                # default rule: s_w >= 512
     A = dev(prob.A)
     fs = float(pl.qn_sum(A, prob.f, prob.fparam).item())
     q = oracle.neumaier(oracle.f_all_meanid_tab(prob))
