@@ -221,12 +221,16 @@ __device__ __constant__ static const double kExp2Tab64[64] = {
 // exp(x) for the elementwise g = exp(p0 y) of C2: x = (k/64) ln 2 + r with
 // |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
 // (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
-// exponent field.  11 fp64 instructions + 1 LDS vs 16 fp64 + branch for exp(); <= ~2.5 ulp.
+// exponent field; <= ~2.5 ulp.  k = rint(64 x / ln 2) by the 1.5 * 2^52 shifter (one DFMA + one DADD,
+// k the low word: no FRND.F64 / F2I.F64 conversions), and the range / NaN handling on the integer
+// bits of x (ALU selects, no DSETP): 10 fp64-pipe instructions + 1 LDS.
 // |x| > 700 is clamped (exp(+-700); the fused kernels' g = exp(p0 y) does not reproduce overflow to inf
-// or underflow to 0 beyond that, include/rqmc.h), NaN propagates (one predicated select).
-__device__ __forceinline__ double exp_t(double x0, const double* etab) {
-  const double x = fmin(fmax(x0, -700.0), 700.0);
-  const double kd = rint(x * 92.33248261689366);                 // 64 / ln 2
+// or underflow to 0 beyond that, include/rqmc.h), NaN propagates.
+__device__ __forceinline__ double exp_t(double x, const double* etab) {
+  constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
+  const double t = fma(x, 92.33248261689366, kShift);            // 64 / ln 2; kShift + rint(64 x / ln 2)
+  const double kd = t - kShift;
+  const int k = __double2loint(t);
   double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
   r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
   double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
@@ -234,10 +238,13 @@ __device__ __forceinline__ double exp_t(double x0, const double* etab) {
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const int k = (int)kd;
   const double v = etab[k & 63] * p;
-  const double e = __longlong_as_double(__double_as_longlong(v) + ((long long)(k >> 6) << 52));
-  return x0 != x0 ? x0 : e;
+  const long long e = __double_as_longlong(v) + ((long long)(k >> 6) << 52);
+  const long long xb = __double_as_longlong(x), ab = xb & 0x7fffffffffffffffLL;
+  // |x| > 700 (bits of 700.0): exp(-700) / exp(700), NaN: x (integer selects, branch-free)
+  const long long sat = xb < 0 ? 0x00d14f2b0fb9307fLL : 0x7f0d945df4f8ec8eLL;
+  const long long big = ab > 0x7ff0000000000000LL ? xb : sat;
+  return __longlong_as_double(ab > 0x4085e00000000000LL ? big : e);
 }
 
 // lane-local sum of g over one leaf node's NV values (reading C-17: 1 identity, 2 exp(p0 y), 3 y^2)

@@ -187,3 +187,27 @@ def test_fine_path_ranks(rq, monkeypatch, cid, G, ck, tmpl, nf):
         pl = _run_case(rq, prob, X, Yo, tmpl, nf, rank=g, world=G)
         tot += float(pl.qn_sum(A, W.F_EXP_MEAN).item())
     check_sum(tot, oracle.f_of_y(Yo, W.F_EXP_MEAN, np.zeros(2)))
+
+
+def test_exp_clamp_fused_tree(rq, monkeypatch):
+    """g = exp(p0 y) in the compile-time trees (exp_t): p0 y beyond 700 is clamped to exp(+-700)
+    (include/rqmc.h, RQMC_F_CALL_MEAN_EXP).  p0 is chosen so ~1e-4 of the entries pass the clamp; the
+    fused f-sum (Y stored and not) equals the clamped definition over the oracle's Y (relative 1e-10:
+    exp amplifies y's 1e-15 relative error by p0 y <= 700)."""
+    monkeypatch.delenv("RQMC_NO_TREE", raising=False)
+    monkeypatch.delenv("RQMC_CKPT_W", raising=False)
+    prob = make_prob(9001, 2, 16, 40, 40, "log")
+    X, Yo = _oracle(prob)
+    p0 = 700.0 / np.quantile(np.abs(Yo), 0.9999)
+    fp = np.array([p0, 1.0])
+    assert (np.abs(p0 * Yo) > 700).sum() > 100
+    fk = np.maximum(np.exp(np.clip(p0 * Yo, -700.0, 700.0)).mean(axis=1) - 1.0, 0.0)
+    q = oracle.neumaier(fk)
+    assert np.isfinite(q)
+    pl = rq.Plan.from_problem(prob)
+    assert pl.dispatch(W.F_CALL_MEAN_EXP, want_y=False).startswith("k_fine_tree<4,2,g=2")
+    A = torch.from_numpy(prob.A).cuda()
+    for want_y in (False, True):
+        fs = pl.xa(A, W.F_CALL_MEAN_EXP, fp)[1] if want_y else pl.qn_sum(A, W.F_CALL_MEAN_EXP, fp)
+        got = float(fs.item())
+        assert abs(got - q) <= 1e-10 * abs(q), (want_y, got, q)
