@@ -128,6 +128,34 @@ def test_identity_matrix_returns_points(rq):
     assert np.array_equal(Yg, X)
 
 
+@pytest.mark.parametrize("kind,b,m,shifted,world", [
+    (W.KIND_LATTICE, 2, 13, True, 1), (W.KIND_LATTICE, 2, 12, False, 1), (W.KIND_LATTICE, 3, 8, True, 1),
+    (W.KIND_NET, 2, 13, True, 1), (W.KIND_NET, 2, 12, False, 1), (W.KIND_MC, 2, 12, False, 1),
+    (W.KIND_NET, 2, 13, True, 3), (W.KIND_LATTICE, 2, 13, True, 4)])
+def test_identity_matrix_mapped_points(rq, kind, b, m, shifted, world):
+    """Phi^-1-mapped points through k_gen (AS 241, tails evaluated from the per-warp queue): with A = I,
+    XA = X exactly, so every row of Y must equal (bit for bit) the same point from rqmc_points (one
+    entry per thread, no queue) and the oracle's points within 4e-15.  A misplaced queued entry, a lost
+    flush or a padding column written as a point fails it.  world > 1: rank 1's rows (the generic loop
+    for nets with grouped classes, nc > 1)."""
+    s = 40
+    prob = W.make_random(31 + kind + 7 * b + m + world, b, m, s, s, kind=kind, shifted=shifted,
+                         mapping=W.MAP_INVNORM)
+    prob.A = np.eye(s)
+    g = 1 if world > 1 else 0
+    pl = rq.Plan.from_problem(prob, rank=g, world=world)
+    Yg = pl.xa(dev(prob.A)).cpu().numpy()
+    ks = pl.global_rows()
+    Xo = oracle.points_rows(prob, ks)
+    np.testing.assert_allclose(Yg, Xo, rtol=4e-15, atol=4e-15)
+    if world == 1:
+        for idx, L in enumerate(pl.levels()):
+            _, vals = pl.points(idx)
+            vals = vals.cpu().numpy()
+            js = slice(L["j_lo"], L["j_lo"] + L["s_w"])
+            assert np.array_equal(Yg[:, js], vals[ks % L["M"]]), f"level {idx}"
+
+
 def test_golden_g1_through_gpu(rq):
     """SURVEY G1 (P:307-309 by hand) through the GPU path, bit-exact."""
     A = np.array([[1, 2], [-1, 0], [2, -3]], dtype=np.float64)
