@@ -14,7 +14,7 @@ LIB = os.path.join(PKG, "librqmc.so")
 SOURCES = [os.path.join(CSRC, f) for f in
            ("rqmc_plan.cpp", "rqmc_gen.cu", "rqmc_gemm.cu", "rqmc_fine.cu", "rqmc_tree.cu", "rqmc_fft.cu")]
 HEADERS = [os.path.join(CSRC, "rqmc_internal.h"), os.path.join(CSRC, "rqmc_device.cuh"),
-           os.path.join(ROOT, "include", "rqmc.h")]
+           os.path.join(CSRC, "rqmc_exp2_table.h"), os.path.join(ROOT, "include", "rqmc.h")]
 DEPS = SOURCES + HEADERS
 OBJDIR = os.path.join(PKG, "build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

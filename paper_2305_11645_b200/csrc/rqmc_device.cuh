@@ -200,6 +200,39 @@ __device__ __forceinline__ double f_of_mean(const FineArgs& a, double mean) {
   }
 }
 
+// a5: fixed-order final reduction fused into the fine kernels (FineArgs::fsum).  Called by every
+// thread of a CTA that has just written its partial (thread 0 wrote it); the last CTA of the replica to
+// arrive sums the replica's nparts partials -- thread t adds partials t, t + NT, ... in order, warps
+// reduce by xor shuffles, thread 0 adds the warp sums in warp order -- so the result does not depend on
+// which CTA arrives last.  Replaces the k_reduce launch (one launch latency on the small configs).
+template <int NT>
+__device__ __forceinline__ void finish_fsum(const FineArgs& a, int64_t rep, int64_t nparts) {
+  if (a.fsum == nullptr) return;
+  __shared__ int s_last;
+  __shared__ double s_red[NT / 32];
+  unsigned int* cnt = a.rcnt + kSplitSlots + rep * 2 * a.partrep;
+  __threadfence();   // the partial is visible device-wide before its arrival is counted
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1u) == (unsigned int)(nparts - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double* p = a.partial + rep * a.partrep;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < nparts; i += NT) s += __ldcg(p + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += s_red[w];
+    RQMC_DCHECK(a.fsum + rep, 8);
+    a.fsum[rep] = t;
+    *cnt = 0u;   // ready for the next call (k_gen zeroes it as well)
+  }
+}
+
 // Y row of local row l (identity, or the residue chunk's row map, FineArgs::ym_nc) and the Y row step
 // per leaf run (see FineArgs::ym_nc): evaluated once per thread
 __device__ __forceinline__ int64_t y_row(const FineArgs& a, int64_t l) {

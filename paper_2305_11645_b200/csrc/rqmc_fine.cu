@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kFineThreads, 1) k_fine(const FineArgs a) {
       RQMC_DCHECK(a.partial + rep * a.partrep + blockIdx.x, 8);
       a.partial[rep * a.partrep + blockIdx.x] = t;
     }
+    finish_fsum<kFineThreads>(a, rep, gridDim.x);
   }
 }
 
@@ -550,7 +551,7 @@ int describe_fine(const FineArgs& a, char* buf, size_t n) {
 }
 
 cudaError_t launch_fine(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st, int64_t* nparts) {
-  *nparts = nb;
+  *nparts = a.fsum ? 0 : nb;   // k_fine ends with finish_fsum (the a5 final reduction) when fsum is set
   if (!no_tree()) {
     const cudaError_t e = launch_tree(a, nb, nrep, st, nparts);
     if (e != cudaErrorNotSupported) return e;

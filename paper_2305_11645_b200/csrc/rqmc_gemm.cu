@@ -379,6 +379,178 @@ static cudaError_t launch_gemm_tma(const GemmArgs& a, int64_t mp_blk, int64_t nu
   return cudaSuccess;
 }
 
+// ------------------------------------------------------------------------------------------
+// Latency-regime variant (levels under one wave of 64 x 64 tiles with <= kLatMacs multiply-adds: C2's
+// coarse chain, C1): a level that small is its launch, load and store latency plus the DMMA chain of
+// one warp (C2's K = 128 level: 32 CTAs of 64 x 64, 512 DMMAs per warp, 9 us).  32 x 32 CTA tiles of
+// 4 warps (2 x 2 warps of 16 x 16 = 2 x 2 DMMA fragments) spread it over 4x the SMs with 4x fewer
+// DMMAs per warp; k-tile 16 on a deep cp.async ring (launch_lat_t).  GATHER: the X operand of merged coarse levels
+// is read from each level's own X^red (GemmArgs::nseg) -- k_gen generates no extra points.  Same
+// accumulation as k_level_gemm (parent row first, k-steps in increasing k).
+// ------------------------------------------------------------------------------------------
+constexpr double kLatMacs = 67108864.0;   // 2^26 multiply-adds (~3.6 us at the fp64 peak)
+
+constexpr int kLatStage = 32 * 20 + 16 * 36;   // doubles per stage: X tile (pitch 20) + A tile (pitch 36)
+
+template <bool GATHER, int CH, int NST>
+__global__ void __launch_bounds__(128) k_level_gemm_lat(const GemmArgs a) {
+  pdl_enter();
+  constexpr int BM = 32, BN = 32, BK = 16, XS = BK + 4, AS = BN + 4;   // pitches: conflict-free
+  extern __shared__ __align__(16) double lsm[];
+  double (*Xs)[BM][XS] = reinterpret_cast<double (*)[BM][XS]>(lsm);
+  double (*As)[BK][AS] = reinterpret_cast<double (*)[BK][AS]>(lsm + NST * BM * XS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, tg = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.y * BM;
+  const int c0 = blockIdx.x * BN;
+  const int64_t zr = blockIdx.z;   // replica: its own X^red and R buffers, shared A
+  const double* __restrict__ Rpg = a.Rp ? a.Rp + zr * a.rrep : nullptr;
+  // loader: X tile 32 x 16 = 256 16-byte chunks, two per thread (rows xr, xr + 16; columns xk, xk + 1);
+  // A tile 16 x 32: CH = 2 two 16-byte chunks per thread (rows ar, ar + 8), CH = 1 four 8-byte elements
+  const int xr = tid >> 3, xk = (tid & 7) * 2;
+  const double* Xb = a.X + zr * a.xrep;
+  // gather: the thread's column q = k0 + xk only moves forward, so its segment and the two row offsets
+  // (row mod M_i) ld_i are recomputed only when q enters the next segment (nseg modulos per thread)
+  int seg = -1;
+  int64_t soff[2] = {0, 0};
+  auto load_stage = [&](int buf, int k0) {
+    const int q = k0 + xk;
+    if constexpr (GATHER) {
+      if (seg < 0 || (seg + 1 < a.nseg && q >= a.segq[seg + 1])) {
+        do { ++seg; } while (seg + 1 < a.nseg && q >= a.segq[seg + 1]);
+        const uint32_t sm = (uint32_t)a.segM[seg];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) soff[u] = (int64_t)((uint32_t)(r0 + xr + 16 * u) % sm) * a.segld[seg];
+      }
+      const double* sx = a.segX[seg] + zr * a.xrep + (q - a.segq[seg]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const bool ok = r0 + xr + 16 * u < a.M && q < a.segq[a.nseg];
+        cp_async16(&Xs[buf][xr + 16 * u][xk], ok ? sx + soff[u] : a.X, ok);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t xrow = r0 + xr + 16 * u;
+        const bool ok = xrow < a.M && q < a.ldx;
+        cp_async16(&Xs[buf][xr + 16 * u][xk], ok ? Xb + xrow * a.ldx + q : a.X, ok);
+      }
+    }
+    if constexpr (CH == 2) {
+      const int ar = tid >> 4, ac = (tid & 15) * 2;
+      const bool cok = c0 + ac < a.tau;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + ar + 8 * u;
+        const bool ok = cok && k < a.K;
+        cp_async16(&As[buf][ar + 8 * u][ac], ok ? a.A + (int64_t)k * a.lda + c0 + ac : a.A, ok);
+      }
+    } else {
+      const int ar = tid >> 5, ac = tid & 31;
+      const bool cok = c0 + ac < a.tau;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + ar + 4 * u;
+        const bool ok = cok && k < a.K;
+        cp_async8(&As[buf][ar + 4 * u][ac], ok ? a.A + (int64_t)k * a.lda + c0 + ac : a.A, ok);
+      }
+    }
+  };
+  const int nk = (a.K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) {
+    if (s < nk) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+  // accumulators start from the parent rows (tile(R_w')) -- loaded while the stages fly
+  double acc[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int64_t row = r0 + wm * 16 + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int col = c0 + wn * 16 + j * 8 + 2 * tg;
+      acc[i][j][0] = 0.0;
+      acc[i][j][1] = 0.0;
+      if (Rpg && row < a.M) {
+        const double* p = Rpg + (int64_t)((uint32_t)row % (uint32_t)a.Mp) * a.ldp + col;   // M < 2^21 here
+        if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
+        if (CH == 2 && col + 1 < a.tau) {
+          const double2 v = *reinterpret_cast<const double2*>(p);
+          acc[i][j][0] = v.x;
+          acc[i][j][1] = v.y;
+        } else {
+          if (col < a.tau) acc[i][j][0] = p[0];
+          if (col + 1 < a.tau) acc[i][j][1] = p[1];
+        }
+      }
+    }
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<NST - 2>();
+    __syncthreads();   // stage kt landed for all threads; stage kt-1's buffer is free
+    if (kt + NST - 1 < nk) load_stage((kt + NST - 1) % NST, (kt + NST - 1) * BK);
+    cp_async_commit();
+    const int buf = kt % NST, kl = a.K - kt * BK;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if (kk < kl) {   // a ragged last tile runs only its valid k-steps
+        double af[2], bf[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) af[i] = Xs[buf][wm * 16 + i * 8 + g][kk + tg];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = As[buf][kk + tg][wn * 16 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  double* R = a.R + zr * a.rrep;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int64_t row = r0 + wm * 16 + i * 8 + g;
+    if (row >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int col = c0 + wn * 16 + j * 8 + 2 * tg;
+      double* p = R + row * a.ldr + col;
+      if (col < a.tau) RQMC_DCHECK(p, col + 1 < a.tau ? 16 : 8);
+      if (CH == 2 && col + 1 < a.tau) {
+        *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (col < a.tau) p[0] = acc[i][j][0];
+        if (col + 1 < a.tau) p[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+// stages: up to 10 k-tiles in flight (K <= 176 resident at once; 107 KB, 2 CTAs per SM) when the level
+// has more than 4 k-tiles -- each k-tile is only 16 DMMAs per warp, so a shallow ring waits one load
+// latency per k-tile (C2's merged K = 193 level: 25 us with 3 stages); 5 stages (48 KB) for K <= 64
+template <bool GATHER, int CH>
+static cudaError_t launch_lat_t(const GemmArgs& a, dim3 grid, cudaStream_t st) {
+  const int nk = (a.K + 15) / 16;
+  auto go = [&](auto kern, int nst) -> cudaError_t {
+    const int sm = nst * kLatStage * (int)sizeof(double);
+    cudaError_t e = set_smem_once(kern, sm);
+    if (e != cudaSuccess) return e;
+    return launch_k(kern, grid, dim3(128), (size_t)sm, st, true, a);
+  };
+  if (nk <= 4) return go(k_level_gemm_lat<GATHER, CH, 5>, 5);
+  return go(k_level_gemm_lat<GATHER, CH, 11>, 11);
+}
+
+static cudaError_t launch_gemm_lat(const GemmArgs& a, int nrep, bool vec, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.tau + 31) / 32), (unsigned)((a.M + 31) / 32), (unsigned)nrep);
+  if (grid.y > 65535) return cudaErrorInvalidValue;
+  if (a.nseg > 0) return vec ? launch_lat_t<true, 2>(a, grid, st) : launch_lat_t<true, 1>(a, grid, st);
+  return vec ? launch_lat_t<false, 2>(a, grid, st) : launch_lat_t<false, 1>(a, grid, st);
+}
+
 template <int BM>
 static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st);
 
@@ -396,6 +568,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st) {
 template <int BM>
 static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) {
   const bool pair = a.Xc != nullptr;
+  if (pair && a.nseg > 0) return cudaErrorNotSupported;   // only k_level_gemm_lat gathers
   const bool vec = ((uintptr_t)a.A % 16 == 0) && (a.lda % 2 == 0) && (a.tau % 2 == 0) &&
                    (!pair || ((uintptr_t)a.Ac % 16 == 0)) &&
                    (a.Rp == nullptr || (((uintptr_t)a.Rp % 16 == 0) && a.ldp % 2 == 0));
@@ -407,6 +580,15 @@ static cudaError_t launch_gemm_bm(const GemmArgs& a, int nrep, cudaStream_t st) 
     nu = (a.M + a.Mp - 1) / a.Mp;
   }
   const int64_t nrb = (mp_blk + BM - 1) / BM * nu;
+  // latency regime (k_level_gemm_lat): under one wave of 64 x 64 tiles and <= kLatMacs, or a gathered
+  // GEMM of merged coarse levels (only that kernel gathers).  RQMC_GEMM_LAT=0 disables (gathered
+  // GEMMs still use it), =1 forces every single-level GEMM onto it.
+  const char* le = std::getenv("RQMC_GEMM_LAT");   // read per launch (tests switch it; graphs capture once)
+  const int lat_mode = le && *le ? std::atoi(le) : -1;
+  const int64_t ncta64 = nrb * ((a.tau + 63) / 64) * nrep;
+  const double macs = (double)a.M * a.tau * a.K * nrep;
+  if (!pair && (a.nseg > 0 || lat_mode == 1 || (lat_mode < 0 && ncta64 < 592 && macs <= kLatMacs)))
+    return launch_gemm_lat(a, nrep, vec, st);
   // TMA tiles for K >= 128 (C5 levels 7..11: 2.01-2.07 vs 2.07-2.10 ms, tensor pipe 93.5-94.7 % vs
   // 91.2-91.8 %: the 128-byte swizzle leaves 2-way bank conflicts on the 8-byte fragment loads
   // (l1tex wavefronts x2), but the loader's address arithmetic disappears (-18 % instructions)); the

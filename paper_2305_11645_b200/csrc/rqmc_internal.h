@@ -17,6 +17,7 @@ constexpr int kSplitSlots = 512;  // max tail bundles split over two CTAs (FineA
 constexpr int kFineBN = 32;       // column tile of the fine kernel
 constexpr int kFinePad = 36;      // padded t / c stride (doubles) of the fine kernel's smem tiles
 constexpr int kFineThreads = 256;
+constexpr int kMaxSeg = 8;        // merged coarse levels per gathered GEMM (GemmArgs::nseg)
 
 // Point-generation view of one level (local rows r'' of this rank).
 struct GenLevel {
@@ -63,6 +64,12 @@ struct GemmArgs {                // one coarse level: R = tile(Rp) + X A_w
   // pair mode (Xc != nullptr): this level's R stays on chip and seeds the next finer level c, whose
   // local rows u M + r (u < ncu) have parent row r; R (this level) is not written, Rc (ldr) is
   const double* Xc; int64_t ldxc; int Kc; const double* Ac; double* Rc; int ncu;
+  // merged coarse levels by gather (Layout::gather): column q of this GEMM's X operand lies in segment
+  // i (segq[i] <= q < segq[i+1]), i.e. at row r mod segM[i], column q - segq[i] of the X^red segX[i]
+  // (leading dimension segld[i]) of one merged level -- the same points (x_{r,j} depends on r mod M_j,
+  // P:307-309) without generating them again at the absorbing level's rows.  nseg = 0: X is one
+  // level's X^red.
+  int nseg; int segq[kMaxSeg + 1]; const double* segX[kMaxSeg]; int64_t segld[kMaxSeg], segM[kMaxSeg];
 };
 
 struct FineLevel {
@@ -94,6 +101,11 @@ struct FineArgs {
   // l = r + j Mroot (Mroot a multiple of ym_nc), i.e. global rows y_row(r) + j ystride with
   // ystride = Mroot (ym_nc = 0) or ym_ncls Mroot / ym_nc: the kernels map once per thread.
   int64_t ym_c0, ym_ncls; int ym_nc;
+  // a5 final reduction fused into the fine kernel (finish_fsum): the last CTA of replica r to write its
+  // partial (arrival counter rcnt[kSplitSlots + r * 2 partrep], zeroed by k_gen every call) adds the
+  // replica's partials in fixed order into fsum[r].  fsum = nullptr: the partials are left for k_reduce.
+  // (One pointer only: ptxas's allocation of the C5 tree is sensitive to this struct's layout.)
+  double* fsum;
 };
 
 // NEXT-4: one FFT-product level (rqmc_fft.cu).  Per valuation v (K = k - v >= 3): L = 2^(K-2) = L1 L2,
@@ -127,7 +139,8 @@ cudaError_t launch_gen(const GenArgs& a, int64_t max_entries, int nrep, cudaStre
 cudaError_t launch_points(const GenArgs& a, int lev, int64_t r0, int64_t count, uint64_t* words,
                           double* vals, cudaStream_t st);
 cudaError_t launch_gemm(const GemmArgs& a, int nrep, cudaStream_t st);
-// nparts: partial sums written per replica (the tree kernel's bundles may be smaller than kBundle;
+// nparts: partial sums left for k_reduce per replica, 0 when the kernel added them itself (finish_fsum)
+// (the tree kernel's bundles may be smaller than kBundle;
 // the workspace holds 4 nbundles partials per replica)
 cudaError_t launch_fine(const FineArgs& a, int64_t nbundles, int nrep, cudaStream_t st, int64_t* nparts);
 // host only: the fine-kernel template launch_fine would pick (for tests / rqmc_plan_dispatch)

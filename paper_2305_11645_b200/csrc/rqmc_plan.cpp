@@ -48,6 +48,7 @@ struct Level {
 struct Layout {
   int ckpt = -1, nfine = 0;
   int absorb = 0;            // levels 0 .. absorb-1 merged into level `absorb` (one GEMM, latency regime)
+  int gather = 0;            // merged levels keep their own X^red; the GEMM gathers (GemmArgs::nseg)
   int64_t nbundles = 0;
   std::vector<Level> lv;     // copy of the plan's levels with coarse / ldx / xoff / rbuf filled
   int ldr = 0;               // row stride of R buffers
@@ -265,12 +266,31 @@ int choose_ckpt(const rqmc_plan_s& p, int64_t reps) {
 // entries under a x 2^20 (unit map; a x 2^17 for reduced-MC draws).  C1: 6 coarse GEMMs -> 1
 // (43.9 -> 18.9 us).  RQMC_ABSORB=0 disables.
 constexpr double kAbsorbMacs = 268435456.0;   // 2^28 (~7 us at the fp64 peak)
+constexpr double kGatherMacs = 67108864.0;    // 2^26: the gathered GEMM stays in k_level_gemm_lat's regime
+// Φ^-1-mapped points merge by gather (Layout::gather): generating the merged columns at level a's rows
+// would evaluate Σ_{i<a} s_i (M_a - M_i) extra Φ^-1 (C2: all coarse levels merged that way 93 -> 112 us,
+// three of five 91 -> 100 us), so the merged levels keep their own X^red and the latency-regime GEMM
+// reads column q of level i at row r mod M_i.  Every merged level but the coarsest must start a 16-byte
+// chunk (even cumulative s_w), and level a's rows fit one grid (<= 2^21).
+int choose_absorb_gather(const rqmc_plan_s& p, const Layout& L, int c, int64_t reps) {
+  int a = 0;
+  for (int i = 1; i <= c && i < kMaxSeg; ++i) {
+    if (L.lv[0].fft || L.lv[i].fft) break;
+    double K = 0.0;
+    bool even = true;
+    for (int q = i; q >= 0; --q) {
+      if (q < i && ((int64_t)K % 2) != 0) even = false;   // segment q starts at column K
+      K += L.lv[q].s_w;
+    }
+    if (!even || L.lv[i].Ml > (int64_t(1) << 21) || (double)L.lv[i].Ml * p.tau * K * reps > kGatherMacs) break;
+    a = i;
+  }
+  return a;
+}
 int choose_absorb(const rqmc_plan_s& p, const Layout& L, int c, int64_t reps) {
   const char* e = std::getenv("RQMC_ABSORB");
   if (e && *e && *e == '0') return 0;
-  // Φ^-1-mapped points: the extra generated entries cost more than the launches saved (C2: all coarse
-  // levels merged 93 -> 112 us, three of five 91 -> 100 us), so only unit-map points merge
-  if (p.map != RQMC_MAP_UNIT) return 0;
+  if (p.map != RQMC_MAP_UNIT) return choose_absorb_gather(p, L, c, reps);
   const double per = p.kind == RQMC_REDUCED_MC ? 131072.0 : 1048576.0;
   int a = 0;
   for (int i = 1; i <= c; ++i) {
@@ -301,6 +321,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L, int64_t reps = 1) {
     V.s_gemm = V.s_w;
   }
   L.absorb = choose_absorb(p, L, c, reps);
+  L.gather = L.absorb > 0 && p.map != RQMC_MAP_UNIT;
   for (int i = 0; i < L.absorb; ++i) {
     L.lv[i].absorbed = 1;
     L.lv[L.absorb].s_gemm += L.lv[i].s_w;   // coarser coordinates follow level a's contiguously in j
@@ -313,10 +334,11 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L, int64_t reps = 1) {
   L.off_x = 0;
   L.max_gen_entries = 0;
   for (auto& V : L.lv) {
-    V.ldx = V.coarse ? (V.s_gemm + 1) / 2 * 2 : V.s_w;
+    V.ldx = V.coarse ? ((L.gather ? V.s_w : V.s_gemm) + 1) / 2 * 2 : V.s_w;
     V.xoff = (int64_t)(off / sizeof(double));
-    if (V.fft || V.absorbed) continue;   // FFT levels need no X^red (H tables in rqmc_fft.cu); merged ones
-                                         // are generated as the absorbing level's columns
+    if (V.fft || (V.absorbed && !L.gather)) continue;   // FFT levels need no X^red (H tables in rqmc_fft.cu);
+                                         // merged ones are generated as the absorbing level's columns
+                                         // (unit map) or keep their own X^red (gather)
     off = align_up(off + (size_t)V.Ml * V.ldx * sizeof(double), 256);
     L.max_gen_entries = std::max<int64_t>(L.max_gen_entries, V.Ml * V.ldx);
   }
@@ -327,7 +349,7 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L, int64_t reps = 1) {
   // 13.54 ms) although it saves R_7's 4.3 GB round trip.  Stored levels alternate R buffers.
   static const bool no_pair = [] { const char* e = std::getenv("RQMC_GEMM_PAIR"); return !(e && *e && *e != '0'); }();
   for (int i = 0; i <= c; ++i) L.lv[i].fused = 0;
-  for (int i = c - 1; i >= L.absorb && !no_pair; i -= 2) {
+  for (int i = c - 1; i >= L.absorb + L.gather && !no_pair; i -= 2) {   // (a gathered GEMM is never a pair)
     const Level &P = L.lv[i], &C = L.lv[i + 1];
     const int64_t ncu = C.Ml / P.Ml;
     if (C.parent == i && ncu * P.Ml == C.Ml && ncu >= 1 && ncu <= 4 && !P.fft && !C.fft) L.lv[i].fused = 1;
@@ -349,7 +371,8 @@ void make_layout(const rqmc_plan_s& p, int c, Layout& L, int64_t reps = 1) {
     const int64_t cap = (int64_t)kSplitSlots * 2 * rows;
     L.split_cap = (p.b == 3 && L.nfine > 0 && cap * 8 <= (int64_t(64) << 20)) ? cap : 0;
     L.off_split = off; off = align_up(off + (size_t)L.split_cap * sizeof(double), 256);
-    L.off_cnt = off; off = align_up(off + (L.split_cap ? (size_t)kSplitSlots * sizeof(unsigned int) : 0), 256);
+    // counters: kSplitSlots split counters, then the fine kernel's arrival counter (finish_fsum)
+    L.off_cnt = off; off = align_up(off + (size_t)(kSplitSlots + 1) * sizeof(unsigned int), 256);
   }
   {  // FFT scratch: sum_v L_v complex per column (ldz = ldr) and per H, for the largest FFT level
     size_t zc = 0, hc = 0;
@@ -787,8 +810,10 @@ GenArgs gen_args(const rqmc_plan_s* p, const Layout& lay, void* work) {
     const Level& L = lay.lv[i];
     int tcl = 0;
     while (tcl < 5 && (1 << tcl) < L.ldx) ++tcl;
-    g.lv[i] = GenLevel{L.M, (L.fft || L.absorbed) ? 0 : L.Ml, L.xoff, L.j_lo, L.s_gemm, L.ldx, tcl,
-                       std::ldexp(1.0, -(p->m - L.w)), (L.coarse && i == (size_t)lay.absorb && lay.absorb > 0) ? 1 : 0};
+    const bool own = lay.gather || !L.absorbed;   // gather: every merged level generates its own X^red
+    g.lv[i] = GenLevel{L.M, (L.fft || !own) ? 0 : L.Ml, L.xoff, L.j_lo, lay.gather ? L.s_w : L.s_gemm, L.ldx, tcl,
+                       std::ldexp(1.0, -(p->m - L.w)),
+                       (!lay.gather && L.coarse && i == (size_t)lay.absorb && lay.absorb > 0) ? 1 : 0};
   }
   return g;
 }
@@ -915,9 +940,8 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
 
   // a2: reduced points of every level (all replicas: grid.z)
   GenArgs g = gen_args(p, lay, w);
-  if (lay.split_cap) {   // k_gen zeroes the fine kernel's split counters (stream order, every call)
-    g.zcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); g.nzcnt = kSplitSlots;
-  }
+  // k_gen zeroes the fine kernel's split and arrival counters (stream order, every call)
+  g.zcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt); g.nzcnt = kSplitSlots + 1;
   g.shift = rr.shift; g.dshift = rr.dshift; g.seeds = rr.seeds; g.srep = rr.srep; g.xrep = rep_d;
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
@@ -939,6 +963,16 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
     }
     a.ldr = lay.ldr;
     a.xrep = rep_d; a.rrep = rep_d;
+    if (lay.gather && i == lay.absorb) {   // merged levels absorb, absorb-1, ..., 0 in increasing j
+      int q = 0;
+      for (int t = i; t >= 0; --t) {
+        const Level& S = lay.lv[t];
+        a.segq[a.nseg] = q; a.segX[a.nseg] = g.X + S.xoff; a.segld[a.nseg] = S.ldx; a.segM[a.nseg] = S.Ml;
+        ++a.nseg;
+        q += S.s_w;
+      }
+      a.segq[a.nseg] = q;
+    }
     if (L.fft) {   // NEXT-4: the level's product by FFTs over the unit group (rqmc_fft.cu); nrep == 1
       const FftArgs fa = fft_args(p, lay, L, w, dA, lda, a.Rp, a.ldp, a.Mp,
                                   reinterpret_cast<double*>(w + lay.off_r[L.rbuf]));
@@ -969,10 +1003,16 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
     if (rqmc_status s = check_cuda(p, e, "chunk fork")) return s;
     st = cx->fine_st;
   }
+  // a5's final fixed-order reduction runs in the fine kernel's last CTA (finish_fsum; k_fine and the
+  // trees with <= 4 fused levels) -- one launch fewer
+  if (want_f) {
+    fa.fsum = d_fsum;
+    fa.rcnt = reinterpret_cast<unsigned int*>(w + lay.off_cnt);   // [kSplitSlots] = the arrival counter
+  }
   int64_t nparts = 0;
   if (rqmc_status s = check_cuda(p, launch_fine(fa, lay.nbundles, nrep, st, &nparts), "k_fine")) return s;
   mark(3);
-  if (want_f)
+  if (want_f && nparts > 0)   // the large trees leave the fixed-order sum of their partials to k_reduce
     if (rqmc_status s = check_cuda(p, launch_reduce(fa.partial, nparts, rep_d, nrep, d_fsum, st), "k_reduce"))
       return s;
   mark(4);

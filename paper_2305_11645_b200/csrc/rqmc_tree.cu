@@ -10,6 +10,7 @@
 #include <type_traits>
 
 #include "rqmc_device.cuh"
+#include "rqmc_exp2_table.h"
 
 namespace rqmc {
 
@@ -30,7 +31,7 @@ namespace rqmc {
 //   K >= 4 levels : DMMA.8x8x4 k-steps (mma.sync f64, C and D in distinct registers); the K = 4
 //                   level's B fragments cached per tile
 //   K = 2 level   : 2 DFMA per output on A values cached in registers per column tile
-//   K = 1 leaves  : 1 DFMA per output, then Y store / g, lane-local sums of g (g = exp: exp_t)
+//   K = 1 leaves  : 1 DFMA per output, then Y store / g, lane-local sums of g (g = exp: exp_core)
 //   row sums      : b = 2: one transpose-reduce over the 4 lanes of a row per 4 NQ leaves; each
 //                   lane keeps complete column-slice sums of its leaf rows in registers across all
 //                   column tiles (no shared-memory row accumulators); other shapes: smem rowacc.
@@ -58,6 +59,9 @@ namespace rqmc {
 #endif
 #ifndef RQMC_TREE_BUNDLE        // residues per CTA: 16 (2 CTAs per SM) or 32 (1 CTA per SM)
 #define RQMC_TREE_BUNDLE 16
+#endif
+#ifndef RQMC_EXP_TB            // exp table bits for g = exp: 6 (64 entries, degree 5) or 11 (2048, degree 3)
+#define RQMC_EXP_TB 6
 #endif
 #ifndef RQMC_TREE_NFR
 #define RQMC_TREE_NFR 4
@@ -218,43 +222,79 @@ __device__ __constant__ static const double kExp2Tab64[64] = {
     1.978456026387951
 };
 
-// exp(x) for the elementwise g = exp(p0 y) of C2: x = (k/64) ln 2 + r with
-// |r| <= ln 2 / 128, exp(x) = 2^(k >> 6) 2^((k & 63)/64) e^r, e^r by its degree-5 Taylor polynomial
-// (truncation < 4e-17), the 2^(j/64) table in shared memory (etab), the power of two added to the
-// exponent field; <= ~2.5 ulp.  k = rint(64 x / ln 2) by the 1.5 * 2^52 shifter (one DFMA + one DADD,
-// k the low word: no FRND.F64 / F2I.F64 conversions), and the range / NaN handling on the integer
-// bits of x (ALU selects, no DSETP): 10 fp64-pipe instructions + 1 LDS.
-// |x| > 700 is clamped (exp(+-700); the fused kernels' g = exp(p0 y) does not reproduce overflow to inf
-// or underflow to 0 beyond that, include/rqmc.h), NaN propagates.
-__device__ __forceinline__ double exp_t(double x, const double* etab) {
-  constexpr double kShift = 6755399441055744.0;                  // 1.5 * 2^52
-  const double t = fma(x, 92.33248261689366, kShift);            // 64 / ln 2; kShift + rint(64 x / ln 2)
+// exp(x) for the elementwise g = exp(p0 y) of C2, table-driven: x = (k / 2^TB) ln 2 + r with
+// |r| <= ln 2 / 2^(TB+1), exp(x) = 2^(k >> TB) 2^((k & (2^TB - 1)) / 2^TB) e^r, the table in shared memory
+// (etab), the power of two added to the exponent field of the high word.  k = rint(2^TB x / ln 2) by the
+// 1.5 * 2^52 shifter (one DFMA + one DADD, k the low word); r by the two-part ln 2 (k ln2_hi exact:
+// |k| < 2^21, ln2_hi has 32 significant bits).  TB = 11 (2048 entries, 16 KB; trees whose shared memory
+// leaves room): |r| <= 1.7e-4, e^r by its degree-3 Taylor polynomial (truncation 3.4e-17): 8 fp64-pipe
+// instructions; TB = 6 (64 entries): degree 5 (truncation < 4e-17), 10.  Both <= ~2 ulp.
+// exp_core has no range handling (valid for |x| <= 700).
+template <int TB>
+__device__ __forceinline__ double exp_core(double x, const double* etab) {
+  static_assert(TB == 6 || TB == 11, "");
+  constexpr double kShift = 6755399441055744.0;                    // 1.5 * 2^52
+  constexpr double kInv = TB == 11 ? 2954.639443740597 : 92.33248261689366;              // 2^TB / ln 2
+  constexpr double kHi = TB == 11 ? 0.00033845077166461124 : 0.01083042469326756;        // ln2_hi / 2^TB
+  constexpr double kLo = TB == 11 ? 9.317455709329042e-14 : 2.9815858269852933e-12;      // ln2_lo / 2^TB
+  const double t = fma(x, kInv, kShift);
   const double kd = t - kShift;
   const int k = __double2loint(t);
-  double r = fma(kd, -0.01083042469326756, x);                    // ln2_hi / 64 (k ln2_hi exact)
-  r = fma(kd, -2.9815858269852933e-12, r);                        // ln2_lo / 64
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const double v = etab[k & 63] * p;
-  const long long e = __double_as_longlong(v) + ((long long)(k >> 6) << 52);
+  double r = fma(kd, -kHi, x);
+  r = fma(kd, -kLo, r);
+  double p;
+  if constexpr (TB == 11) {
+    p = fma(r, 1.0 / 6.0, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+  } else {
+    p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+  }
+  const double v = etab[k & ((1 << TB) - 1)] * p;
+  return __hiloint2double(__double2hiint(v) + ((k >> TB) << 20), __double2loint(v));
+}
+// |x| > 700 or NaN, on the high word (the range exp_core does not handle)
+__device__ __forceinline__ bool exp_out_of_range(double x) {
+  return (unsigned)(__double2hiint(x) & 0x7fffffff) > 0x4085e000u;
+}
+// exp_core with the range handling: |x| > 700 is clamped (exp(+-700); the fused kernels' g = exp(p0 y)
+// does not reproduce overflow to inf or underflow to 0 beyond that, include/rqmc.h), NaN propagates
+// (integer selects on the bits of x, branch-free)
+template <int TB>
+__device__ __forceinline__ double exp_t(double x, const double* etab) {
+  const long long e = __double_as_longlong(exp_core<TB>(x, etab));
   const long long xb = __double_as_longlong(x), ab = xb & 0x7fffffffffffffffLL;
-  // |x| > 700 (bits of 700.0): exp(-700) / exp(700), NaN: x (integer selects, branch-free)
-  const long long sat = xb < 0 ? 0x00d14f2b0fb9307fLL : 0x7f0d945df4f8ec8eLL;
+  const long long sat = xb < 0 ? 0x00d14f2b0fb9307fLL : 0x7f0d945df4f8ec8eLL;   // exp(-700) / exp(700)
   const long long big = ab > 0x7ff0000000000000LL ? xb : sat;
   return __longlong_as_double(ab > 0x4085e00000000000LL ? big : e);
 }
 
 // lane-local sum of g over one leaf node's NV values (reading C-17: 1 identity, 2 exp(p0 y), 3 y^2)
-template <int G, int NV>
+// (g = exp: exp_core per value and one warp vote per node; a warp that saw |p0 y| > 700 or a NaN
+// recomputes the node with exp_t's range handling -- identical bits for the in-range values.  Range
+// selects on every value had cost 9 of C2's 36 instructions per output.)
+template <int G, int NV, int TB>
 __device__ __forceinline__ double gsum(const double (&S)[NV], double p0, const double* etab) {
   if constexpr (G == 2) {
 #if RQMC_FAST_EXP
-    double v = exp_t(p0 * S[0], etab);
+    double x = p0 * S[0];
+    bool bad = exp_out_of_range(x);
+    double v = exp_core<TB>(x, etab);
 #pragma unroll
-    for (int e = 1; e < NV; ++e) v += exp_t(p0 * S[e], etab);
+    for (int e = 1; e < NV; ++e) {
+      x = p0 * S[e];
+      bad |= exp_out_of_range(x);
+      v += exp_core<TB>(x, etab);
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      v = exp_t<TB>(p0 * S[0], etab);
+#pragma unroll
+      for (int e = 1; e < NV; ++e) v += exp_t<TB>(p0 * S[e], etab);
+    }
 #else
     double v = exp(p0 * S[0]);
 #pragma unroll
@@ -306,6 +346,10 @@ struct TreeRun {
   static constexpr int RW = NQ;                                    // leaf row sums a lane keeps per block
   static constexpr int NACC = kRegAcc ? NBAT * RW : 1;
   static constexpr int K1 = (B == 2 && NF >= 2) ? T::K(NF - 2) : 0;  // the K = 2 level (b = 2)
+  // exp table bits (g = exp): 64 entries.  The 2048-entry table (16 KB, degree-3 polynomial: 8 instead of
+  // 10 fp64 instructions) measured slower on C2 (fine 35.3 -> 38.0 us, C2 x 64 1.61 -> 1.69 ms): random
+  // lookups into 16 KB hit more shared-memory bank conflicts than into 512 B (RQMC_EXP_TB=11 to A/B)
+  static constexpr int TB = (RQMC_EXP_TB == 11 && G == 2 && T::SMEM + 2048 * 8 <= 112 * 1024) ? 11 : 6;
 
   const FineArgs& a;
   const TreeCtx& c;
@@ -313,7 +357,7 @@ struct TreeRun {
   double a1[K1 == 2 ? 2 : 1][NV];                       // A values of the K = 2 level (DFMA)
   double b4[RQMC_CACHE_B4 && kB2 ? NFR : 1];            // B fragments of the K = 4 level (one DMMA k-step)
   double racc[NACC];                                    // row sums sum_c g(y_kc) of this lane's leaf rows
-  const double* etab = nullptr;                         // g = exp: 2^(j/64) table in shared memory
+  const double* etab = nullptr;                         // g = exp: 2^(j/2^TB) table in shared memory
 
   __device__ __forceinline__ TreeRun(const FineArgs& a_, const TreeCtx& c_) : a(a_), c(c_) {
 #pragma unroll
@@ -364,7 +408,7 @@ struct TreeRun {
         tree_step<KL, NFR, T::XP, T::AP>(xs(I, j), as(I), c, Sp, Y);
       }
       tree_store<STY, NFR>(a, Y, j, c);
-      if constexpr (G > 0) v[q] = gsum<G, NV>(Y, a.fp0, etab);
+      if constexpr (G > 0) v[q] = gsum<G, NV, TB>(Y, a.fp0, etab);
     }
     if constexpr (G > 0) {
 #pragma unroll
@@ -451,7 +495,7 @@ struct TreeRun {
 #pragma unroll
           for (int e = 0; e < NV; ++e) Y[e] = fma(x0, a0[0][e], S1[e]);
           tree_store<STY, NFR>(a, Y, jl[l], c);
-          if constexpr (G > 0) v[l] = gsum<G, NV>(Y, a.fp0, etab);
+          if constexpr (G > 0) v[l] = gsum<G, NV, TB>(Y, a.fp0, etab);
         }
       }
     }
@@ -529,6 +573,9 @@ struct TreeRun {
     level<0, 0>(Sroot, 0);
   }
 };
+
+template <int NF>
+constexpr bool kFuseReduce = NF <= 4;   // trees that end with finish_fsum (the a5 final reduction)
 
 template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
@@ -646,9 +693,13 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
   };
 
   Run run(a, c);
-  if constexpr (G == 2) {   // exp_t's table, visible after the barrier below
-    __shared__ double etab[64];
-    if (tid < 64) etab[tid] = kExp2Tab64[tid];
+  if constexpr (G == 2) {   // exp's table, visible after the barrier below
+    __shared__ double etab[1 << Run::TB];
+    if constexpr (Run::TB == 11) {
+      for (int i = tid; i < 2048; i += NT) etab[i] = kExp2Tab2048[i];
+    } else {
+      if (tid < 64) etab[tid] = kExp2Tab64[tid];
+    }
     run.etab = etab;
   }
   load_tile(ct_lo & 1, ct_lo * CW);
@@ -741,6 +792,9 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
       RQMC_DCHECK(a.partial + rep * a.partrep + bundle, 8);
       a.partial[rep * a.partrep + bundle] = t;
     }
+    // (small trees only: in the NF >= 5 trees the extra code perturbs ptxas's allocation of the hot loop
+    // -- C5 fine 16.9 -> 18.4 ms -- where one k_reduce launch is 0.01 % of the step)
+    if constexpr (kFuseReduce<NF>) finish_fsum<NT>(a, rep, (a.Mroot + BUN - 1) / BUN);
   }
 }
 
@@ -805,7 +859,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   if (e != cudaSuccess) return e;
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
-  *nparts = nbt;
+  *nparts = (kFuseReduce<NF> && a.fsum) ? 0 : nbt;   // 0: the kernel wrote the f-sum itself
   FineArgs b = a;
   b.nfull = tree_split_first<NF, B, G, STY>(a, nbt);
   b.nsplit = b.nfull < nbt ? 2 : 1;
