@@ -27,10 +27,15 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB, defines=()) -> bool:
+    """lib missing, older than a source / header, or (variants) built with other -D flags."""
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    if lib != LIB:
+        stamp = lib + ".defs"
+        if not os.path.exists(stamp) or open(stamp).read() != " ".join(defines):
+            return True
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
@@ -57,8 +62,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     (loaded only when RQMC_LIB points at it)."""
     lib = LIB if not variant else os.path.join(PKG, f"librqmc_{variant}.so")
     objdir = OBJDIR if not variant else os.path.join(OBJDIR, variant)
-    if not variant and not force and not needs_build():
-        return LIB
+    if not force and not needs_build(lib, defines):
+        return lib
     os.makedirs(objdir, exist_ok=True)
     if force:
         for f in os.listdir(objdir):
@@ -72,6 +77,9 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking librqmc.so")
     os.replace(lib + ".tmp", lib)
+    if variant:
+        with open(lib + ".defs", "w") as fh:
+            fh.write(" ".join(defines))
     return lib
 
 

@@ -4,7 +4,8 @@ librqmc_debug.so is the same library compiled with -DRQMC_DEBUG=1: every cp.asyn
 global store of the path (k_gen X^red, GEMM R tiles and parent rows, fine-kernel X^red / A / root loads,
 Y stores, partials, tail-split scratch, FFT R rows) is checked against the buffers of the run and a
 violation traps.  This test re-runs a cross-section of the parity suites -- every fused-fine kernel
-template, the b = 3 tail split, batches, the residue partition, the FFT levels -- against that library
+template, the b = 3 tail split, batches, the residue partition, the FFT levels, the latency-regime and
+gathered coarse GEMMs -- against that library
 (RQMC_LIB) in a subprocess; any out-of-bounds access fails it.
 """
 import os
@@ -24,6 +25,7 @@ def test_parity_subset_under_bounds_checks():
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
            os.path.join(ROOT, "tests", "test_gpu_fine_paths.py"), os.path.join(ROOT, "tests", "test_gpu_parity.py"),
            os.path.join(ROOT, "tests", "test_gpu_batch.py"), os.path.join(ROOT, "tests", "test_gpu_fft.py"),
+           os.path.join(ROOT, "tests", "test_gpu_latency.py"),
            "-k", "not config and not qn_host and not pair_fusion and not sweep and not graph and not exact"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
