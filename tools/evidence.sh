@@ -1,5 +1,6 @@
 # Evidence pass (round 2): bench lines of every config, launch list and ncu summaries of C5,
-# the C4 fine kernel, the torchrun / gloo multi-rank dry runs and the simulated scaling.
+# the C4 fine kernel, the C2 latency-regime kernels, kernel timelines of the small configs, the
+# torchrun / gloo multi-rank dry runs and the simulated scaling.
 # usage (on the GPU box): bash tools/evidence.sh r02a
 P=${1:-r02}
 set -x
@@ -16,12 +17,16 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ev/plain_lau
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ev/${P}_launches_C5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ev/ncu_launch.log 2>&1
 python tools/prof_step.py --config C5 > gpurun_out/ev/plain_full.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:'k_fine_tree|k_level_gemm|k_gen' -s 8 -c 9 -o gpurun_out/ev/${P}_C5_full python tools/prof_step.py --config C5 > gpurun_out/ev/ncu_full.log 2>&1
+for c in C1 C2; do python tools/timeline.py --config $c --steps 2 > gpurun_out/ev/${P}_timeline_$c.txt 2>/dev/null; done
+python tools/prof_step.py --config C2 > gpurun_out/ev/plain_c2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:'k_fine_tree|k_level_gemm_lat|k_gen' -s 12 -c 5 -o gpurun_out/ev/${P}_C2_full python tools/prof_step.py --config C2 --steps 1 --warmup 2 > gpurun_out/ev/ncu_c2.log 2>&1
 python tools/prof_step.py --config C4 --xa > gpurun_out/ev/plain_c4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:'k_fine_tree' -c 1 -o gpurun_out/ev/${P}_C4_tree python tools/prof_step.py --config C4 --xa > gpurun_out/ev/ncu_c4.log 2>&1
 ls -la gpurun_out/ev
 # summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit)
 python tools/ncu_summary.py launches gpurun_out/ev/${P}_launches_C5.csv "# ncu launch list, python bench.py --steps 2 --warmup 3 --no-cpu-baseline (C5), gpu__time_duration.sum, --clock-control none; cold-cache, serialised: compare SHARES" > gpurun_out/ev/${P}_launches_C5_summary.txt
 python tools/ncu_summary.py full gpurun_out/ev/${P}_C5_full.ncu-rep "# ncu --set full --clock-control none --import-source on -k regex:'k_fine_tree|k_level_gemm|k_gen' -s 8 -c 9, tools/prof_step.py --config C5 (one step)" > gpurun_out/ev/${P}_ncu_C5_kernels.txt
+python tools/ncu_summary.py full gpurun_out/ev/${P}_C2_full.ncu-rep "# ncu --set full, k_gen / k_level_gemm_lat / k_fine_tree of tools/prof_step.py --config C2 (one step)" > gpurun_out/ev/${P}_ncu_C2_kernels.txt
 python tools/ncu_summary.py full gpurun_out/ev/${P}_C4_tree.ncu-rep "# ncu --set full, k_fine_tree of tools/prof_step.py --config C4 --xa (Y stored)" > gpurun_out/ev/${P}_ncu_C4_tree.txt
 mkdir -p /tmp/ncurep && mv gpurun_out/ev/*.ncu-rep /tmp/ncurep/
 du -sh gpurun_out
