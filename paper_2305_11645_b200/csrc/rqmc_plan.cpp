@@ -163,6 +163,11 @@ struct rqmc_plan_s {
   std::mutex h2d_mu;
   cudaStream_t h2d_stream = nullptr;
   cudaEvent_t h2d_ev[2] = {nullptr, nullptr};
+  // A arrives in the order the run reads it: one copy (and event) per coarse level, then the fine rows
+  std::vector<cudaEvent_t> h2d_lv_ev;   // per level index; the last entry: the fine levels' rows
+  double* h_fsum_pin = nullptr;         // pinned landing slot of the f-sum (graph-captured host runs)
+  struct HostGraph { const void *hA, *dwork; int64_t lda; int f; double fp0, fp1; cudaGraphExec_t exec; };
+  std::vector<HostGraph> host_graphs;
   cudaError_t up_err = cudaSuccess;
   uint64_t* d_z = nullptr;
   double* d_shift = nullptr;
@@ -696,6 +701,10 @@ void rqmc_plan_destroy(rqmc_plan_t p) {
   for (auto e : p->h2d_ev)
     if (e) cudaEventDestroy(e);
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
+  for (auto e : p->h2d_lv_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& hg : p->host_graphs) cudaGraphExecDestroy(hg.exec);
+  if (p->h_fsum_pin) cudaFreeHost(p->h_fsum_pin);
   for (auto& ge : p->graphs) cudaGraphExecDestroy(ge.exec);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->d_z) cudaFree(p->d_z);
@@ -908,7 +917,8 @@ struct ChunkCtx {
 };
 
 rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_t rep_bytes, const RunRand& rr,
-                     cudaEvent_t a_ready /* nullable: A is produced on another stream; wait before the GEMMs */,
+                     const cudaEvent_t* a_ready /* nullable: A arrives on another stream; [i] before coarse
+                                                   level i reads its rows, [nl] before the fine levels */,
                      const double* dA,
                      int64_t lda, double* dY, int64_t ldy, rqmc_f f, const double* fparam, double* d_fsum,
                      cudaStream_t st, const ChunkCtx* cx = nullptr) {
@@ -946,14 +956,14 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   if (rqmc_status s = check_cuda(p, launch_gen(g, lay.max_gen_entries, nrep, st), "k_gen")) return s;
   mark(1);
   phase.next("rqmc:a3+a4 coarse levels (k_level_gemm / k_fft)");
-  if (a_ready)
-    if (rqmc_status s = check_cuda(p, cudaStreamWaitEvent(st, a_ready, 0), "wait for A")) return s;
 
   // a3+a4 coarse levels: R_w = tile(R_w') + X_w A_w, coarse -> fine.  A fused pair (Layout) runs as
   // one launch whose parent R never leaves the chip (bit-identical to two launches).
   for (int i = 0; i <= lay.ckpt; ++i) {
     const Level& L = lay.lv[i];
     if (L.absorbed) continue;    // merged into level lay.absorb's GEMM
+    if (a_ready && a_ready[i])   // this level's rows of A have landed
+      if (rqmc_status s = check_cuda(p, cudaStreamWaitEvent(st, a_ready[i], 0), "wait for A")) return s;
     GemmArgs a{};
     a.X = g.X + L.xoff; a.ldx = L.ldx; a.M = L.Ml; a.K = L.s_gemm;
     a.A = dA + (int64_t)L.j_lo * lda; a.lda = lda; a.tau = p->tau;
@@ -995,6 +1005,8 @@ rqmc_status run_core(rqmc_plan_s* p, const Layout& lay, int nrep, char* w, size_
   phase.next("rqmc:a3-a5 fused fine levels + f (k_fine, k_reduce)");
 
   // a3+a4+a5 fine levels fused with f / Y store
+  if (a_ready && a_ready[lay.lv.size()])
+    if (rqmc_status s = check_cuda(p, cudaStreamWaitEvent(st, a_ready[lay.lv.size()], 0), "wait for A")) return s;
   FineArgs fa = fine_args(p, lay, w, g.X, dA, lda, dY, ldy, want_f ? (int)f : -1, fparam, rep_d);
   if (cx) {   // chunk: continue on the fine stream once the coarse levels are done
     fa.ym_c0 = cx->ym_c0; fa.ym_ncls = cx->ym_ncls; fa.ym_nc = cx->ym_nc;
@@ -1143,6 +1155,42 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
   return run(p, dA, lda, nullptr, 0, f, fparam, d_fsum, dwork, wbytes, static_cast<cudaStream_t>(stream));
 }
 
+// H2D of A in the order the run reads it -- each coarse level's rows (coarse -> fine), then the fine
+// levels' rows -- on the copy stream, one event per piece: the first GEMM waits for its own rows only,
+// the later copies overlap the GEMMs before them (C3: the 8 MB of A took 0.26 ms before the first GEMM).
+static cudaError_t issue_h2d(rqmc_plan_s* p, const double* hA, int64_t lda, double* dA, cudaStream_t st) {
+  const Layout& L = p->L1;
+  const size_t nl = L.lv.size();
+  cudaError_t e = cudaEventRecord(p->h2d_ev[0], st);   // after earlier work on st: A's buffer is free
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h2d_stream, p->h2d_ev[0], 0);
+  int jmin = p->s;
+  static const bool one_piece = [] { const char* v = std::getenv("RQMC_H2D_ONE"); return v && *v && *v != '0'; }();
+  if (one_piece) {   // A/B: all of A in one copy, every level waits for it
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(dA, (size_t)L.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
+                            (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, p->h2d_stream);
+    for (size_t i = 0; i <= nl && e == cudaSuccess; ++i) e = cudaEventRecord(p->h2d_lv_ev[i], p->h2d_stream);
+    return e;
+  }
+  auto copy = [&](int j0, int nj, cudaEvent_t ev) {
+    if (e != cudaSuccess) return;
+    if (nj > 0)
+      e = cudaMemcpy2DAsync(dA + (int64_t)j0 * L.ldr, (size_t)L.ldr * sizeof(double), hA + (int64_t)j0 * lda,
+                            (size_t)lda * sizeof(double), (size_t)p->tau * sizeof(double), (size_t)nj,
+                            cudaMemcpyHostToDevice, p->h2d_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, p->h2d_stream);
+  };
+  for (size_t i = 0; i <= (size_t)L.ckpt && i < nl; ++i) {
+    const Level& V = L.lv[i];
+    if (V.absorbed) continue;
+    const int nj = std::min(V.fft ? V.s_w : V.s_gemm, p->s - V.j_lo);
+    copy(V.j_lo, nj, p->h2d_lv_ev[i]);
+    jmin = std::min(jmin, V.j_lo);
+  }
+  copy(0, jmin, p->h2d_lv_ev[nl]);   // the fine levels' rows (j < the finest coarse level's first row)
+  return e;
+}
+
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream) {
   if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
@@ -1155,29 +1203,69 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
   char* w = static_cast<char*>(dwork);
   double* dA = reinterpret_cast<double*>(w + p->L1.off_a);
   double* dsum = reinterpret_cast<double*>(w + p->L1.off_fsum);
-  // H2D of A on a copy stream, overlapped with the point generation (which does not read A); the
-  // GEMMs wait for it.  Ordered after earlier work on st (ev[0]) so A's staging buffer is free.
   std::lock_guard<std::mutex> lk(p->h2d_mu);
   cudaError_t e = cudaSuccess;
+  const size_t nl = p->L1.lv.size();
   if (!p->h2d_stream) {
     e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&p->h2d_ev[i], cudaEventDisableTiming);
+    p->h2d_lv_ev.assign(nl + 1, nullptr);
+    for (size_t i = 0; i <= nl && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&p->h2d_lv_ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost(&p->h_fsum_pin, sizeof(double));
     if (rqmc_status s = check_cuda(p, e, "copy stream")) return s;
   }
-  e = cudaEventRecord(p->h2d_ev[0], st);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h2d_stream, p->h2d_ev[0], 0);
-  if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(dA, (size_t)p->L1.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
-                          (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, p->h2d_stream);
-  if (e == cudaSuccess) e = cudaEventRecord(p->h2d_ev[1], p->h2d_stream);
-  if (rqmc_status s = check_cuda(p, e, "H2D A")) return s;
   const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
-  if (rqmc_status s = run_core(p, p->L1, 1, w, p->L1.off_fsum, rr, p->h2d_ev[1], dA, p->L1.ldr, nullptr, 0, f, fparam,
-                               dsum, st))
-    return s;
-  e = cudaMemcpyAsync(h_fsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
+  auto sequence = [&](double* out_host) -> rqmc_status {
+    if (rqmc_status s = check_cuda(p, issue_h2d(p, hA, lda, dA, st), "H2D A")) return s;
+    if (rqmc_status s = run_core(p, p->L1, 1, w, p->L1.off_fsum, rr, p->h2d_lv_ev.data(), dA, p->L1.ldr, nullptr,
+                                 0, f, fparam, dsum, st))
+      return s;
+    return check_cuda(p, cudaMemcpyAsync(out_host, dsum, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H fsum");
+  };
+  // Page-locked A (the bench's pinned buffer): the whole sequence -- the copy-stream fork, the piecewise
+  // H2D, the kernels, the D2H into a pinned slot -- is captured once as a CUDA graph and replayed (the
+  // small configs are dominated by ~10 launches from the host otherwise).  Pageable A runs directly.
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, hA) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  static const bool no_graph = RQMC_DEBUG || [] { const char* v = std::getenv("RQMC_NO_GRAPH"); return v && *v && *v != '0'; }();
+  if (!pinned || no_graph || p->prof_max > 0) {
+    if (rqmc_status s = sequence(h_fsum)) return s;
+    return check_cuda(p, cudaStreamSynchronize(st), "D2H fsum");
+  }
+  const double fp0 = fparam ? fparam[0] : 0.0, fp1 = fparam ? fparam[1] : 0.0;
+  cudaGraphExec_t exec = nullptr;
+  for (auto& hg : p->host_graphs)
+    if (hg.hA == hA && hg.dwork == dwork && hg.lda == lda && hg.f == (int)f && hg.fp0 == fp0 && hg.fp1 == fp1)
+      exec = hg.exec;
+  if (!exec) {
+    if (!p->cap_stream) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (rqmc_status s = check_cuda(p, e, "capture")) return s;
+    cudaStream_t keep = st;
+    st = p->cap_stream;
+    const rqmc_status s = sequence(p->h_fsum_pin);
+    st = keep;
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(p->cap_stream, &graph);
+    if (s == RQMC_OK && e == cudaSuccess && graph) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (s != RQMC_OK || e != cudaSuccess || !exec) {   // run directly
+      cudaGetLastError();
+      if (rqmc_status s2 = sequence(h_fsum)) return s2;
+      return check_cuda(p, cudaStreamSynchronize(st), "D2H fsum");
+    }
+    if (p->host_graphs.size() >= 8) {
+      cudaGraphExecDestroy(p->host_graphs.front().exec);
+      p->host_graphs.erase(p->host_graphs.begin());
+    }
+    p->host_graphs.push_back({hA, dwork, lda, (int)f, fp0, fp1, exec});
+  }
+  e = cudaGraphLaunch(exec, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  return check_cuda(p, e, "D2H fsum");
+  if (rqmc_status s = check_cuda(p, e, "host graph")) return s;
+  *h_fsum = *p->h_fsum_pin;
+  return RQMC_OK;
 }
 
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes) {

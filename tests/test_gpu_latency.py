@@ -136,3 +136,22 @@ def test_latency_gemm_forced(rq, monkeypatch, seed, b, m, s, tau, kind, shifted,
         ks = np.arange(prob.N)
         check_rows(prob, Y.cpu().numpy(), ks)
         check_fsum(prob, float(fs.item()), ks)
+
+
+@pytest.mark.parametrize("config", ["C1", "C3"])
+def test_qn_host_pinned_and_pageable(rq, config):
+    """rqmc_qn_host: A copied per level in the order the run reads it (the GEMMs wait for their own rows);
+    with page-locked A the whole sequence is a replayed CUDA graph.  Both forms, repeated and with a
+    second buffer, equal the device-resident run bit for bit."""
+    prob = W.make_config(config)
+    pl = rq.Plan.from_problem(prob)
+    ref = float(pl.qn_sum(dev(prob.A), prob.f, prob.fparam).item())
+    pin = torch.from_numpy(prob.A.copy()).pin_memory()
+    pin2 = torch.from_numpy(prob.A.copy()).pin_memory()
+    for _ in range(3):
+        assert pl.qn_host(pin.numpy(), prob.f, prob.fparam) == ref
+    assert pl.qn_host(pin2.numpy(), prob.f, prob.fparam) == ref
+    assert pl.qn_host(np.array(prob.A, copy=True), prob.f, prob.fparam) == ref   # pageable: direct launches
+    pin.numpy()[:] = 0.0   # the replayed graph reads the buffer's current contents
+    z = float(pl.qn_sum(dev(np.zeros_like(prob.A)), prob.f, prob.fparam).item())
+    assert pl.qn_host(pin.numpy(), prob.f, prob.fparam) == z
