@@ -6,6 +6,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -855,7 +856,11 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   if constexpr (T::SMEM > 227 * 1024) {
     return cudaErrorNotSupported;
   }
-  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, T::SMEM);
+  // A/B experiments only: RQMC_FINE_SMEM_KB pads the dynamic shared memory (fewer fine CTAs per SM,
+  // e.g. to leave room for concurrent GEMM CTAs of the residue-chunk pipeline)
+  static const int pad_kb = [] { const char* v = std::getenv("RQMC_FINE_SMEM_KB"); return v && *v ? std::atoi(v) : 0; }();
+  const int smem = std::max<int>(T::SMEM, pad_kb * 1024);
+  cudaError_t e = set_smem_once(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, smem);
   if (e != cudaSuccess) return e;
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
@@ -865,7 +870,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   b.nsplit = b.nfull < nbt ? 2 : 1;
   const int64_t grid = b.nfull + (nbt - b.nfull) * b.nsplit;
   return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)grid, (unsigned)nrep), dim3(T::THREADS),
-                  (size_t)T::SMEM, st, false, b);
+                  (size_t)smem, st, false, b);
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
