@@ -130,8 +130,10 @@ typedef struct {
   int coarse;       /* 1: materialised per-level GEMM pass; 0: fused into the fine kernel      */
   int fft;          /* 1: coarse level computed by the FFT product over the unit group of
                        Z / 2^k (unshifted b = 2 lattices, NEXT-4)   */
-  int absorbed;     /* 1: coarse level merged into a finer coarse level's GEMM (small unit-map
-                       problems: one launch for several levels; same points)       */
+  int absorbed;     /* 1: coarse level merged into a finer coarse level's GEMM (small problems:
+                       one launch for several levels; same points, P:307-309 -- unit map: the
+                       merged columns generated at the absorbing level's rows; Phi^-1 map: each
+                       level keeps its own reduced points, the GEMM reads level i at row r mod M_i) */
 } rqmc_level_info;
 
 typedef struct {
@@ -178,8 +180,11 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
 
 /* End-to-end form with HOST buffers: copies hA (pinned or pageable) into the workspace, runs
  * rqmc_qn and copies the local f-sum back into *h_fsum; synchronises the stream before returning.
- * The H2D copy of A runs on a plan-owned copy stream, overlapped with the point generation (which
- * does not read A); the GEMMs wait for it (full overlap needs pinned hA).  Not reentrant per plan
+ * The H2D copy of A runs on a plan-owned copy stream in the order the run reads it (each coarse
+ * level's rows, coarse to fine, then the fine levels' rows), overlapped with the point generation and
+ * the GEMMs before it: each GEMM waits only for its own rows.  With page-locked hA the whole sequence
+ * (copies, kernels, the D2H into a plan-owned pinned slot) is captured once per (hA, lda, f, fparam,
+ * dwork) as a CUDA graph and replayed; the replay reads hA's current contents.  Not reentrant per plan
  * (serialised by a plan mutex). */
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream);
