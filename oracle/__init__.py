@@ -52,6 +52,8 @@ def lib():
         dp, u64p, i64p = C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
         _lib.orc_invnorm.restype = C.c_double
         _lib.orc_invnorm.argtypes = [C.c_double]
+        _lib.orc_tent.restype = C.c_double
+        _lib.orc_tent.argtypes = [C.c_double]
         _lib.orc_points.argtypes = [C.POINTER(_Prob), C.c_int64, C.c_int64, dp, u64p]
         _lib.orc_product.argtypes = [C.c_int64, C.c_int, C.c_int, dp, dp, dp]
         _lib.orc_f.argtypes = [C.c_int64, C.c_int, dp, C.c_int, dp, dp]
@@ -120,6 +122,11 @@ def mc_points_bank(prob, bank_cols, k0: int = 0, n: int | None = None) -> np.nda
     X = np.empty((n, prob.s), dtype=np.float64)
     lib().orc_mc_points_bank(C.byref(h.s), _ptr(bank, C.c_double), _ptr(off, C.c_int64), k0, n, _ptr(X, C.c_double))
     return X
+
+
+def tent(u: float) -> float:
+    """phi(u) = 1 - |1 - 2u|, the oracle's C evaluation."""
+    return lib().orc_tent(float(u))
 
 
 def invnorm(u: float) -> float:

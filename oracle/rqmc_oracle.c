@@ -17,7 +17,8 @@
  *        reduced MC (Eq. randpts) x_{j,n} = y_{j, m_s N_{s+1} + ... + m_j N_{j+1}} from the
  *                 mixed-radix digits of n; the bank y_{j,r} is the counter-based stream of include/rqmc.h
  *        row-zeroed net (kind 3): the same definition with any C^(j) (no column deletion assumed)
- *        map      x = Phi^-1(u), zero rule reading C-5
+ *        map      x = Phi^-1(u), zero rule reading C-5; or the tent
+ *                 transformation phi(u) = 1 - |1 - 2u|
  *   O2 product Y[k,c] = sum_{j=1..s} x_{k,j} A[j,c], increasing j
  *   O3 f_k = F(tau^-1 sum_c g(Y[k,c])) (increasing c); sum_k f_k Neumaier-compensated
  *   O3' (g = id only) f_k = F(sum_j x_{k,j} abar_j), abar = tau^-1 A 1   -- algebraic identity, O(Ns)
@@ -41,7 +42,7 @@ typedef struct {
   const uint64_t* C;       /* net: column words, C[j*m+q] bit (m-1-p) = C^(j)_{p+1,q+1} */
   const double* shift;     /* lattice Delta_j in [0,1) or NULL */
   const uint64_t* dshift;  /* net sigma_j < 2^53 or NULL */
-  int map;                 /* 0 identity, 1 Phi^-1 */
+  int map;                 /* 0 identity, 1 Phi^-1, 2 tent */
   uint64_t seed;           /* kind 2 (reduced Monte Carlo): seed of the counter-based draws */
 } orc_problem;
 
@@ -74,9 +75,14 @@ double orc_invnorm(double u) {
   return u < 0.5 ? x : -x;
 }
 
-/* u in [0,1) -> point coordinate, with the zero rule (reading C-5). */
+/* The tent transformation phi(x) = 1 - |1 - 2x| (the alternative to the random
+ * shift), evaluated as written: 2x, 1 - 2x, |.|, 1 - |.| in fp64 (2x is exact). */
+double orc_tent(double u) { return 1.0 - fabs(1.0 - 2.0 * u); }
+
+/* u in [0,1) -> point coordinate: identity, Phi^-1 with the zero rule (reading C-5), or the tent map. */
 static double orc_map(const orc_problem* p, double u, int shifted) {
   if (p->map == 0) return u;
+  if (p->map == 2) return orc_tent(u);
   if (u == 0.0) u = shifted ? ldexp(1.0, -53) : 0.5 / (double)ipow((uint64_t)p->b, p->m);
   return orc_invnorm(u);
 }
@@ -143,7 +149,7 @@ static double orc_mc_value(const orc_problem* p, int j, uint64_t idx, uint64_t* 
   const uint64_t word = orc_mc_word(p->seed, j, idx);
   if (word_out) *word_out = word;
   const double u = (double)(word | 1u) * ldexp(1.0, -53);    /* in (0,1): no zero rule needed */
-  return p->map == 0 ? u : orc_invnorm(u);
+  return p->map == 0 ? u : (p->map == 2 ? orc_tent(u) : orc_invnorm(u));
 }
 
 /* O1 for one entry: coordinate j of point k (value, and its integer word in *word). */

@@ -170,6 +170,32 @@ def test_lattice_periodicity_multiplicity_and_means(b, m, s):
             assert np.all(X[:, jj] == 0.0)               # j > s*: zero column
 
 
+@pytest.mark.parametrize("b,m,s", [(2, 8, 20), (3, 5, 14), (5, 3, 9)])
+def test_tent_map_definition_and_means(b, m, s):
+    """Tent transformation phi(x) = 1 - |1 - 2x| (the alternative to the random shift):
+    phi(0) = 0, phi(1/4) = phi(3/4) = 1/2, phi(1/2) = 1.  An unshifted reduced lattice column is a
+    permutation of the grid {t / M_j}, so its tent-mapped mean is sum_t phi(t/M)/M = 1/2 for
+    even M and 1/2 - 1/(2 M^2) for odd M (pairs t, M - t; 0 for M = 1), and the map acts entry by entry on
+    the unmapped points (by exact rationals for b = 2, where t/M is dyadic)."""
+    assert (oracle.tent(0.0), oracle.tent(0.25), oracle.tent(0.5), oracle.tent(0.75)) == (0.0, 0.5, 1.0, 0.5)
+    w = W.w_log(b, m, s)
+    z = W.draw_z(7, b, m, w)
+    X, _ = oracle.points(lattice(b, m, w, z, mapping=W.MAP_TENT))
+    Xu, _ = oracle.points(lattice(b, m, w, z))
+    N = b ** m
+    for j in range(s):
+        Mj = b ** (m - min(int(w[j]), m))
+        exp = Fr(1, 2) if Mj % 2 == 0 else Fr(1, 2) - Fr(1, 2 * Mj * Mj)
+        assert abs(math.fsum(X[:, j]) / N - float(exp)) <= 1e-15
+        assert np.array_equal(X[:, j], np.tile(X[:Mj, j], N // Mj))
+        for k in range(0, N, max(1, N // 37)):
+            t = 1 - abs(1 - 2 * Fr(Xu[k, j]))
+            if b == 2:
+                assert Fr(X[k, j]) == t
+            else:
+                assert abs(Fr(X[k, j]) - t) <= Fr(1, 2 ** 52)
+
+
 def test_shifted_means_closed_form():
     """psi(x) = {x + Delta}: mean of M equispaced shifted values = (1-1/M)/2 + {M Delta}/M."""
     b, m, s = 2, 9, 40

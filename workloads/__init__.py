@@ -163,7 +163,7 @@ def a_kl(s: int, tau: int) -> np.ndarray:
 # f ids (match include/rqmc.h rqmc_f)
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
 KIND_LATTICE, KIND_NET, KIND_MC, KIND_NET_ROWS = 0, 1, 2, 3
-MAP_UNIT, MAP_INVNORM = 0, 1
+MAP_UNIT, MAP_INVNORM, MAP_TENT = 0, 1, 2   # TENT: phi(x) = 1 - |1 - 2x|
 
 
 @dataclasses.dataclass
