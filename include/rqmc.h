@@ -86,7 +86,12 @@ typedef enum {
 typedef enum {
   RQMC_LATTICE = 0, RQMC_DIGITAL_NET = 1, RQMC_REDUCED_MC = 2, RQMC_DIGITAL_NET_ROWS = 3
 } rqmc_kind;
-typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1 } rqmc_map;
+/* Point map applied to every coordinate u in [0,1): identity; Phi^-1 (the Gaussian workloads,
+ * P:59-67; u = 0 remapped, reading C-5); or the tent transformation phi(u) = 1 - |1 - 2u| (P:250-253:
+ * "the random shift can be replaced by the tent transformation"; evaluated as written in fp64, 2u exact,
+ * so GPU and oracle agree bit for bit).  The map commutes with the reduction: coordinate j still depends
+ * on k mod M_j only. */
+typedef enum { RQMC_MAP_UNIT = 0, RQMC_MAP_INVNORM = 1, RQMC_MAP_TENT = 2 } rqmc_map;
 
 /* f(y) = F(tau^-1 sum_c g(y_c))  (SURVEY reading C-17)                                    */
 typedef enum {

@@ -25,7 +25,7 @@ from ._build import LIB as _LIB_PATH
 _LIB_PATH = os.environ.get("RQMC_LIB", _LIB_PATH)
 
 LATTICE, DIGITAL_NET, REDUCED_MC, DIGITAL_NET_ROWS = 0, 1, 2, 3
-MAP_UNIT, MAP_INVNORM = 0, 1
+MAP_UNIT, MAP_INVNORM, MAP_TENT = 0, 1, 2
 F_NONE, F_EXP_MEAN, F_CALL_MEAN_EXP, F_MEAN_SQ, F_MEAN = -1, 0, 1, 2, 3
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPRIME", 3: "EWORDER", 4: "EZUNIT", 5: "ESHIFT", 6: "ENETMAT",

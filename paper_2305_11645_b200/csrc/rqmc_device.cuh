@@ -200,6 +200,12 @@ __device__ __forceinline__ double f_of_mean(const FineArgs& a, double mean) {
   }
 }
 
+// The tent transformation phi(u) = 1 - |1 - 2u|, evaluated as written with
+// round-to-nearest adds (2u exact): the oracle's orc_tent bit for bit.
+__device__ __forceinline__ double tent_map(double u) {
+  return __dadd_rn(1.0, -fabs(__dadd_rn(1.0, __dmul_rn(-2.0, u))));
+}
+
 // a5: fixed-order final reduction fused into the fine kernels (FineArgs::fsum).  Called by every
 // thread of a CTA that has just written its partial (thread 0 wrote it); the last CTA of the replica to
 // arrive sums the replica's nparts partials -- thread t adds partials t, t + NT, ... in order, warps

@@ -67,12 +67,15 @@ __device__ __forceinline__ uint32_t pow5(int e, int K) {            // 5^e mod 2
   return (uint32_t)(K >= 32 ? r : (r & ((1ull << K) - 1)));
 }
 
-// phi(t / 2^k): identity or Phi^-1 with the zero rule (unshifted lattice levels only)
+// phi(t / 2^k): identity, Phi^-1 with the zero rule, or the tent map (unshifted lattice levels only;
+// one map for every coordinate of the level)
 __device__ __forceinline__ double fft_phi(const FftArgs& a, uint64_t t) {
   double u = (double)(uint32_t)t * a.inv_M;
   if (a.map == 1) {
     if (u == 0.0) u = a.zero_u;
     u = normcdfinv(u);
+  } else if (a.map == 2) {
+    u = tent_map(u);
   }
   return u;
 }

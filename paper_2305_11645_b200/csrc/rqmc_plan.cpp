@@ -503,7 +503,7 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
     return bad(RQMC_EINVAL, "bad kind");
   // row-zeroed net (Alg. 3/4): the same generator as a net; only the level table differs
   const bool rowzero = d->kind == RQMC_DIGITAL_NET_ROWS;
-  if (d->map != RQMC_MAP_UNIT && d->map != RQMC_MAP_INVNORM) return bad(RQMC_EINVAL, "bad map");
+  if (d->map != RQMC_MAP_UNIT && d->map != RQMC_MAP_INVNORM && d->map != RQMC_MAP_TENT) return bad(RQMC_EINVAL, "bad map");
   if (d->m * std::log2((double)d->b) > 32.0 + 1e-9) return bad(RQMC_EUNSUPPORTED, "N = b^m > 2^32");
   if ((d->kind == RQMC_DIGITAL_NET || rowzero) && (d->b != 2 || d->m > 32))
     return bad(RQMC_EUNSUPPORTED, "digital nets need b = 2, m <= 32");
@@ -622,9 +622,10 @@ rqmc_status rqmc_plan_create(const rqmc_plan_desc* d, rqmc_plan_t* out) {
       int j2 = j;
       while (j2 < d->s && level_of(j2) == wl) ++j2;
       // columns j > s* are x = 0: dropped, unless a shift or the map makes them the
-      // constant phi_j(Delta_j) / Phi^-1(zero rule) -- then a 1-row level m (reading C-4)
+      // constant phi_j(Delta_j) / Phi^-1(zero rule) -- then a 1-row level m (reading C-4); the tent
+      // map keeps 0 at 0 (phi(0) = 0), so unshifted tent columns are dropped like unit-map ones
       // (reduced MC: N_j = 1 for w_j >= m -- one i.i.d. draw per coordinate, P:981 N_{s+1} = 1)
-      if (wl < d->m || p->shifted || d->map != RQMC_MAP_UNIT || d->kind == RQMC_REDUCED_MC) {
+      if (wl < d->m || p->shifted || d->map == RQMC_MAP_INVNORM || d->kind == RQMC_REDUCED_MC) {
         Level L{};
         L.w = wl; L.j_lo = j; L.s_w = j2 - j; L.fft_tab = -1;
         L.M = ipow(d->b, d->m - wl);
