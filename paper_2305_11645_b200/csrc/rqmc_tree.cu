@@ -575,6 +575,26 @@ struct TreeRun {
   }
 };
 
+// Phase clock (A/B builds with -DRQMC_TREE_CLOCK=1 only): thread 0 of CTA x records %globaltimer at
+// entry, after the prologue, after each tile and at the end into g_tree_clk[x][0..15]
+// (tools/tree_clock.py reads it through rqmc_debug_tree_clock).
+#ifndef RQMC_TREE_CLOCK
+#define RQMC_TREE_CLOCK 0
+#endif
+#if RQMC_TREE_CLOCK
+constexpr int kClkCtas = 8192, kClkSlots = 16;
+__device__ unsigned long long g_tree_clk[kClkCtas * kClkSlots];
+__device__ __forceinline__ void tree_clk(int slot) {
+  if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < kClkCtas && slot < kClkSlots) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tree_clk[blockIdx.x * kClkSlots + slot] = t;
+  }
+}
+#else
+__device__ __forceinline__ void tree_clk(int) {}
+#endif
+
 template <int NF>
 constexpr bool kFuseReduce = NF <= 4;   // trees that end with finish_fsum (the a5 final reduction)
 
@@ -582,6 +602,7 @@ template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
     k_fine_tree(const FineArgs a) {
   pdl_enter();
+  tree_clk(0);
   using T = Tree<NF, B, NFR, BUN, NH>;
   using Run = TreeRun<NF, B, G, STY, NFR, BUN, NH>;
   constexpr int NT = T::THREADS, NW = T::WARPS;
@@ -631,6 +652,10 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
   }
   cp_async_commit();
+#if RQMC_TREE_CLOCK >= 2
+  cp_async_wait<0>();   // phase split (clock builds only): X^red subtree landed
+  tree_clk(12);
+#endif
   if constexpr (G > 0 && !Run::kRegAcc)
     for (int e = tid; e < T::ACCN; e += NT) fsm[T::ACC + e] = 0.0;
 
@@ -703,9 +728,13 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
     run.etab = etab;
   }
+#if RQMC_TREE_CLOCK >= 2
+  tree_clk(13);
+#endif
   load_tile(ct_lo & 1, ct_lo * CW);
   cp_async_wait<0>();  // X^red subtree and the first tile resident
   __syncthreads();
+  tree_clk(1);
   const int cw0 = c.cw;
   for (int ct = ct_lo; ct < ct_hi; ++ct) {
     c.c0 = ct * CW;
@@ -720,6 +749,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
     cp_async_wait<0>();
     __syncthreads();  // tile ct + 1 landed and visible; buffers (ct & 1) free for tile ct + 2
+    tree_clk(2 + ct - ct_lo);
   }
 
   if constexpr (G > 0) {
@@ -797,6 +827,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     // -- C5 fine 16.9 -> 18.4 ms -- where one k_reduce launch is 0.01 % of the step)
     if constexpr (kFuseReduce<NF>) finish_fsum<NT>(a, rep, (a.Mroot + BUN - 1) / BUN);
   }
+  tree_clk(15);
 }
 
 // residues per CTA: b = 3 trees run 3 warp groups (one per top-level run; 2 groups split the 3 runs
@@ -945,6 +976,19 @@ cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st
     default: return cudaErrorNotSupported;
   }
 }
+
+#if RQMC_TREE_CLOCK
+}  // namespace rqmc
+extern "C" int rqmc_debug_tree_clock(unsigned long long* out, int n) {   // A/B builds only
+  if (n > rqmc::kClkCtas * rqmc::kClkSlots) n = rqmc::kClkCtas * rqmc::kClkSlots;
+  return (int)cudaMemcpyFromSymbol(out, rqmc::g_tree_clk, (size_t)n * sizeof(unsigned long long));
+}
+extern "C" int rqmc_debug_tree_clock_reset() {
+  static unsigned long long z[rqmc::kClkCtas * rqmc::kClkSlots];
+  return (int)cudaMemcpyToSymbol(rqmc::g_tree_clk, z, sizeof(z));
+}
+namespace rqmc {
+#endif
 
 #if RQMC_DEBUG
 cudaError_t dbg_set_tree(const DbgRanges& r, cudaStream_t st) { return dbg_set_tu(r, st); }
