@@ -69,3 +69,14 @@ def test_tent_ranks(rq, G):
         check_rows(prob, Y.cpu().numpy(), np.asarray(p.global_rows()))
         tot += float(fs.item())
     check_fsum(prob, tot, np.arange(prob.N))
+
+
+def test_tent_batch(rq):
+    """Batched shifts with the tent map: each replica equals the oracle's f-sum of that shift."""
+    import dataclasses
+    prob = W.make_random(360, 2, 12, 80, 48, shifted=True, mapping=W.MAP_TENT, f=W.F_EXP_MEAN)
+    pl = rq.Plan.from_problem(prob)
+    shifts = np.random.default_rng(3).random((3, prob.s))
+    got = pl.qn_batch(dev(prob.A), prob.f, prob.fparam, shifts=shifts).cpu().numpy()
+    for r in range(3):
+        check_fsum(dataclasses.replace(prob, shift=shifts[r]), float(got[r]), np.arange(prob.N))
