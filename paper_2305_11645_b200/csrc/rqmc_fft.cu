@@ -4,7 +4,8 @@
 // i.e. no per-coordinate shift).
 //
 // Level w has M = 2^k distinct rows; its points are x_{r,j} = phi((r z'_j mod M) / M) with
-// one map phi (identity or Phi^-1 with the zero rule, reading C-5) for all coordinates j of the level.
+// one map phi (identity, Phi^-1 with the zero rule, reading C-5, or the tent map) for all
+// coordinates j of the level.
 // Split the rows by 2-adic valuation: r = 2^v u, u odd, K = k - v.  For K >= 3 the odd residues mod 2^K
 // form {+-1} x <5> (5 has order L = 2^(K-2)), so u = sigma 5^e and z'_j = sigma_j 5^(e_j) (mod 2^K):
 //   P[2^v sigma 5^e, c] = sum_{sigma'} sum_{e'} H_v(sigma sigma', e + e') a_v(sigma', e', c),

@@ -276,7 +276,7 @@ constexpr double kGatherMacs = 67108864.0;    // 2^26: the gathered GEMM stays i
 // would evaluate Σ_{i<a} s_i (M_a - M_i) extra Φ^-1 (C2: all coarse levels merged that way 93 -> 112 us,
 // three of five 91 -> 100 us), so the merged levels keep their own X^red and the latency-regime GEMM
 // reads column q of level i at row r mod M_i.  Every merged level but the coarsest must start a 16-byte
-// chunk (even cumulative s_w), and level a's rows fit one grid (<= 2^21).
+// chunk (even cumulative s_w), and level a's rows fit one grid (< 2^21: 32-row tiles, grid.y <= 65535).
 int choose_absorb_gather(const rqmc_plan_s& p, const Layout& L, int c, int64_t reps) {
   int a = 0;
   for (int i = 1; i <= c && i < kMaxSeg; ++i) {
@@ -287,7 +287,7 @@ int choose_absorb_gather(const rqmc_plan_s& p, const Layout& L, int c, int64_t r
       if (q < i && ((int64_t)K % 2) != 0) even = false;   // segment q starts at column K
       K += L.lv[q].s_w;
     }
-    if (!even || L.lv[i].Ml > (int64_t(1) << 21) || (double)L.lv[i].Ml * p.tau * K * reps > kGatherMacs) break;
+    if (!even || L.lv[i].Ml >= (int64_t(1) << 21) || (double)L.lv[i].Ml * p.tau * K * reps > kGatherMacs) break;
     a = i;
   }
   return a;
