@@ -1175,7 +1175,10 @@ static cudaError_t issue_h2d(rqmc_plan_s* p, const double* hA, int64_t lda, doub
   }
   auto copy = [&](int j0, int nj, cudaEvent_t ev) {
     if (e != cudaSuccess) return;
-    if (nj > 0)
+    if (nj > 0 && lda == L.ldr)   // equal pitches: one linear copy
+      e = cudaMemcpyAsync(dA + (int64_t)j0 * L.ldr, hA + (int64_t)j0 * lda, (size_t)nj * lda * sizeof(double),
+                          cudaMemcpyHostToDevice, p->h2d_stream);
+    else if (nj > 0)
       e = cudaMemcpy2DAsync(dA + (int64_t)j0 * L.ldr, (size_t)L.ldr * sizeof(double), hA + (int64_t)j0 * lda,
                             (size_t)lda * sizeof(double), (size_t)p->tau * sizeof(double), (size_t)nj,
                             cudaMemcpyHostToDevice, p->h2d_stream);
