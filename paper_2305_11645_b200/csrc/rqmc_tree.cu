@@ -595,8 +595,10 @@ __device__ __forceinline__ void tree_clk(int slot) {
 __device__ __forceinline__ void tree_clk(int) {}
 #endif
 
-template <int NF>
-constexpr bool kFuseReduce = NF <= 4;   // trees that end with finish_fsum (the a5 final reduction)
+// trees that end with finish_fsum (the a5 final reduction): the small b = 2 trees (C2's latency
+// regime); the b = 3 trees (C4: one k_reduce launch is 3 us of 4.5 ms) keep their round-1 code
+template <int NF, int B>
+constexpr bool kFuseReduce = NF <= 4 && B == 2;
 
 template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
@@ -825,7 +827,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
     // (small trees only: in the NF >= 5 trees the extra code perturbs ptxas's allocation of the hot loop
     // -- C5 fine 16.9 -> 18.4 ms -- where one k_reduce launch is 0.01 % of the step)
-    if constexpr (kFuseReduce<NF>) finish_fsum<NT>(a, rep, (a.Mroot + BUN - 1) / BUN);
+    if constexpr (kFuseReduce<NF, B>) finish_fsum<NT>(a, rep, (a.Mroot + BUN - 1) / BUN);
   }
   tree_clk(15);
 }
@@ -895,7 +897,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   if (e != cudaSuccess) return e;
   const int64_t nbt = (a.Mroot + BUN - 1) / BUN;   // bundles of BUN residues (partials written)
   if (nbt > 4 * nb) return cudaErrorInvalidValue;   // workspace holds 4 nb partials per replica
-  *nparts = (kFuseReduce<NF> && a.fsum) ? 0 : nbt;   // 0: the kernel wrote the f-sum itself
+  *nparts = (kFuseReduce<NF, B> && a.fsum) ? 0 : nbt;   // 0: the kernel wrote the f-sum itself
   FineArgs b = a;
   b.nfull = tree_split_first<NF, B, G, STY>(a, nbt);
   b.nsplit = b.nfull < nbt ? 2 : 1;
