@@ -576,7 +576,7 @@ struct TreeRun {
 };
 
 // Phase clock (A/B builds with -DRQMC_TREE_CLOCK=1 only): thread 0 of CTA x records %globaltimer at
-// entry, after the prologue, after each tile and at the end into g_tree_clk[x][0..15]
+// entry, after the prologue, after each of the first 10 tiles and at the end into g_tree_clk[x][0..15]
 // (tools/tree_clock.py reads it through rqmc_debug_tree_clock).
 #ifndef RQMC_TREE_CLOCK
 #define RQMC_TREE_CLOCK 0
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
     cp_async_wait<0>();
     __syncthreads();  // tile ct + 1 landed and visible; buffers (ct & 1) free for tile ct + 2
-    tree_clk(2 + ct - ct_lo);
+    if (ct - ct_lo < 10) tree_clk(2 + ct - ct_lo);   // slots 2..11 (12, 13: CLOCK=2 sub-phases; 15: end)
   }
 
   if constexpr (G > 0) {

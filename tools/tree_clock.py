@@ -4,7 +4,7 @@
     RQMC_LIB=$PWD/paper_2305_11645_b200/librqmc_clk.so RQMC_NO_GRAPH=1 python tools/tree_clock.py --config C2
 
 Thread 0 of each CTA records %globaltimer at entry (slot 0), after the prologue (X^red subtree and the
-first column tile resident, slot 1), after every column tile (slots 2..) and at the end (slot 15).
+first column tile resident, slot 1), after each of the first 10 column tiles (slots 2..11; later tiles count into the epilogue) and at the end (slot 15).
 Prints the distribution of start times, prologue, per-tile and epilogue durations (us).
 """
 import argparse
@@ -47,17 +47,17 @@ def main():
     q = lambda v: f"p0 {np.min(v):.2f} p50 {np.median(v):.2f} p90 {np.percentile(v, 90):.2f} max {np.max(v):.2f}"
     start = (t[:, 0] - t0) / 1e3
     pro = (t[:, 1] - t[:, 0]) / 1e3
-    ntile = int(np.max(np.sum(t[:, 2:15] > 0, axis=1)))
+    ntile = int(np.max(np.sum(t[:, 2:12] > 0, axis=1)))
     last = t[:, 1 + ntile]
     tiles = np.diff(t[:, 1:2 + ntile], axis=1) / 1e3
     epi = (t[:, 15] - last) / 1e3
     end = (t[:, 15] - t0) / 1e3
-    print(f"# {args.config}: {len(t)} CTAs, {ntile} column tiles each; kernel span {end.max():.2f} us")
+    print(f"# {args.config}: {len(t)} CTAs, {ntile} column tiles recorded each (at most 10); kernel span {end.max():.2f} us")
     print("start  ", q(start))
     print("prolog ", q(pro))
     for i in range(ntile):
         print(f"tile {i} ", q(tiles[:, i]))
-    print("epilog ", q(epi))
+    print("epilog " if ntile < 10 else "tiles>=10 + epilog ", q(epi))
     if np.all(t[:, 12] > 0):   # RQMC_TREE_CLOCK=2: X^red landed (12), first tile issued (13)
         print("  X^red load  ", q((t[:, 12] - t[:, 0]) / 1e3))
         print("  etab / setup", q((t[:, 13] - t[:, 12]) / 1e3))
