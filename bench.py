@@ -277,9 +277,9 @@ def main():
             return fsum.cpu().numpy()
         if Y is None:   # C ABI rqmc_qn_host: H2D of A and D2H of the f-sum inside the call
             return plan.qn_host(A_host, prob.f, prob.fparam)
-        A_e2e.copy_(A_pin, non_blocking=True)   # XA configs: Y stays a device-resident output
-        plan.xa(A_e2e, prob.f, prob.fparam, Y=Y, fsum=fsum)
-        return float(fsum.item())
+        # XA configs: C ABI rqmc_xa_host (A's H2D overlapped with the run, f-sum back to host);
+        # Y stays a device-resident output
+        return plan.xa_host(A_host, Y, prob.f, prob.fparam)
 
     for _ in range(2):
         e2e_call()
@@ -388,8 +388,9 @@ def main():
         "phases_ms_per_step": {k: v / runs for k, v in prof.items() if k.endswith("_ms")},
         "e2e": {"value": R * prob.N * prob.tau / (e2e_tot / args.steps * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(prob.s * prob.tau * 8), "d2h_bytes_per_step": 8 * R,
-                "api": "rqmc_qn_host (pinned host A -> device, local f-sum -> host)" if Y is None else
-                       "Plan.xa (pinned host A -> device copy, Y device-resident output, f-sum -> host)"},
+                "api": ("Plan.qn_batch (pinned host A -> device copy, R local f-sums -> host)" if R > 1 else
+                        "rqmc_qn_host (pinned host A -> device, local f-sum -> host)" if Y is None else
+                        "rqmc_xa_host (pinned host A -> device, Y device-resident output, local f-sum -> host)")},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "qn": qn_val,

@@ -194,6 +194,16 @@ rqmc_status rqmc_qn(rqmc_plan_t p, const double* dA, int64_t lda, rqmc_f f, cons
 rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
                          double* h_fsum, void* dwork, size_t wbytes, void* stream);
 
+/* rqmc_xa with A in HOST memory (pinned or pageable), the same piecewise overlapped H2D and graph
+ * replay as rqmc_qn_host: Y = X A on this rank's rows into the caller's DEVICE buffer dY (ldy >= tau;
+ * an N x tau result of up to tens of GB stays in HBM), and, if f != RQMC_F_NONE, the local f-sum into
+ * *h_fsum (required then).  Synchronises the stream before returning.  The opt-in residue-chunk
+ * pipeline (RQMC_CHUNKS) is not used here.  Errors: EINVAL (null hA / dY / dwork, f without h_fsum,
+ * workspace too small), EDIM (lda or ldy < tau), ECUDA. */
+rqmc_status rqmc_xa_host(rqmc_plan_t p, const double* hA, int64_t lda, double* dY, int64_t ldy,
+                         rqmc_f f, const double* fparam, double* h_fsum, void* dwork, size_t wbytes,
+                         void* stream);
+
 /* Batched randomisation: R independent randomisations of
  * the SAME plan (generating vector / matrices, layout, map) and the same A, each giving its own
  * local f-sum:  d_fsum[r] = sum over this rank's rows of f(x^(r)_k^T A), r = 0..R-1 (device array).

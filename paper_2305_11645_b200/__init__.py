@@ -66,7 +66,7 @@ class Summary(C.Structure):
 
 EXPORTS = ["rqmc_plan_create", "rqmc_plan_destroy", "rqmc_strerror", "rqmc_plan_last_error",
            "rqmc_plan_summary_get", "rqmc_plan_level", "rqmc_plan_global_row", "rqmc_plan_stats",
-           "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_points",
+           "rqmc_workspace_size", "rqmc_xa", "rqmc_qn", "rqmc_qn_host", "rqmc_xa_host", "rqmc_points",
            "rqmc_profile_enable", "rqmc_profile_read", "rqmc_workspace_size_batch", "rqmc_qn_batch",
            "rqmc_plan_summary_batch", "rqmc_plan_dispatch", "rqmc_plan_partition"]
 
@@ -97,6 +97,7 @@ def lib():
         L.rqmc_xa.argtypes = [vp, vp, i64, vp, i64, C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_qn.argtypes = [vp, vp, i64, C.c_int, dp, vp, vp, C.c_size_t, vp]
         L.rqmc_qn_host.argtypes = [vp, dp, i64, C.c_int, dp, dp, vp, C.c_size_t, vp]
+        L.rqmc_xa_host.argtypes = [vp, dp, i64, vp, i64, C.c_int, dp, dp, vp, C.c_size_t, vp]
         L.rqmc_points.argtypes = [vp, C.c_int, i64, i64, vp, vp, vp]
         L.rqmc_profile_enable.argtypes = [vp, C.c_int]
         L.rqmc_workspace_size_batch.argtypes = [vp, C.c_int, C.POINTER(C.c_size_t)]
@@ -323,6 +324,26 @@ class Plan:
                                        _p(fp, C.c_double), C.byref(out), C.c_void_p(ws.data_ptr()),
                                        ws.numel(), _stream_ptr(stream)))
         return out.value
+
+    def xa_host(self, A_host: np.ndarray, Y, f: int = F_NONE, fparam=None, stream=None):
+        """End-to-end XA: host A in (H2D inside the C call, overlapped with the run), Y = X A into the
+        device tensor Y (N_local x tau, unit column stride); with f, returns the local f-sum (host float)."""
+        import torch
+        A_host = np.asarray(A_host)
+        if A_host.dtype != np.float64 or A_host.shape != (self.s, self.tau) or not A_host.flags.c_contiguous:
+            raise ValueError("A_host must be a C-contiguous float64 s x tau array")
+        nl = self.summary()["N_local"]
+        if not (isinstance(Y, torch.Tensor) and Y.is_cuda and Y.dtype == torch.float64 and Y.dim() == 2
+                and Y.shape[0] == nl and Y.shape[1] == self.tau and Y.stride(1) == 1):
+            raise ValueError(f"Y must be a CUDA float64 {nl} x {self.tau} tensor with unit column stride")
+        ws = self.workspace(Y.device)
+        fp = _arr(fparam if fparam is not None else [0.0, 0.0], np.float64)
+        out = C.c_double()
+        self._check(lib().rqmc_xa_host(self._h, A_host.ctypes.data_as(C.POINTER(C.c_double)), self.tau,
+                                       C.c_void_p(Y.data_ptr()), Y.stride(0), f, _p(fp, C.c_double),
+                                       C.byref(out) if f != F_NONE else None, C.c_void_p(ws.data_ptr()),
+                                       ws.numel(), _stream_ptr(stream)))
+        return out.value if f != F_NONE else None
 
     def points(self, level_idx: int, r0: int = 0, count: Optional[int] = None):
         """Reduced points of one level: (integer words, fp64 values), each count x s_w."""

@@ -166,7 +166,7 @@ struct rqmc_plan_s {
   // A arrives in the order the run reads it: one copy (and event) per coarse level, then the fine rows
   std::vector<cudaEvent_t> h2d_lv_ev;   // per level index; the last entry: the fine levels' rows
   double* h_fsum_pin = nullptr;         // pinned landing slot of the f-sum (graph-captured host runs)
-  struct HostGraph { const void *hA, *dwork; int64_t lda; int f; double fp0, fp1; cudaGraphExec_t exec; };
+  struct HostGraph { const void *hA, *dwork; const void* dY; int64_t lda, ldy; int f; double fp0, fp1; cudaGraphExec_t exec; };
   std::vector<HostGraph> host_graphs;
   cudaError_t up_err = cudaSuccess;
   uint64_t* d_z = nullptr;
@@ -1165,8 +1165,12 @@ static cudaError_t issue_h2d(rqmc_plan_s* p, const double* hA, int64_t lda, doub
   cudaError_t e = cudaEventRecord(p->h2d_ev[0], st);   // after earlier work on st: A's buffer is free
   if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h2d_stream, p->h2d_ev[0], 0);
   int jmin = p->s;
-  static const bool one_piece = [] { const char* v = std::getenv("RQMC_H2D_ONE"); return v && *v && *v != '0'; }();
-  if (one_piece) {   // A/B: all of A in one copy, every level waits for it
+  // Small A (C1 8 KB, C2 512 KB) goes in one copy: each piece costs a copy's fixed latency, more than
+  // the overlap gains (e2e C1 86 -> 59 us, C2 139 -> 132 us; C3 / C4 keep the pieces: 1.09 -> 1.01 ms,
+  // 5.72 -> 5.30 ms; profiles/r02f_h2d_pieces_ab.txt).  RQMC_H2D_ONE=0/1 forces either form.
+  static const int one_env = [] { const char* v = std::getenv("RQMC_H2D_ONE"); return v && *v ? (*v != '0') : -1; }();
+  const bool one_piece = one_env >= 0 ? one_env == 1 : (double)p->s * p->tau * sizeof(double) < 2.0 * (1 << 20);
+  if (one_piece) {   // all of A in one copy, every level waits for it
     if (e == cudaSuccess)
       e = cudaMemcpy2DAsync(dA, (size_t)L.ldr * sizeof(double), hA, (size_t)lda * sizeof(double),
                             (size_t)p->tau * sizeof(double), (size_t)p->s, cudaMemcpyHostToDevice, p->h2d_stream);
@@ -1195,13 +1199,15 @@ static cudaError_t issue_h2d(rqmc_plan_s* p, const double* hA, int64_t lda, doub
   return e;
 }
 
-rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
-                         double* h_fsum, void* dwork, size_t wbytes, void* stream) {
-  if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+// Host-buffer runs (rqmc_qn_host, rqmc_xa_host): A from host memory (piecewise H2D on the copy stream,
+// overlapped with the run), Y (xa only) into the caller's device buffer, the local f-sum back to host.
+static rqmc_status run_host(rqmc_plan_s* p, const double* hA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                            const double* fparam, double* h_fsum, void* dwork, size_t wbytes, void* stream) {
   if (wbytes < p->L1.total) return fail(p, RQMC_EINVAL, "workspace too small");
-  if (lda < p->tau) return fail(p, RQMC_EDIM, "lda < tau");
-  if (f == RQMC_F_NONE) return fail(p, RQMC_EINVAL, "rqmc_qn_host needs f");
+  if (lda < p->tau || (dY && ldy < p->tau)) return fail(p, RQMC_EDIM, "lda/ldy < tau");
   if (rqmc_status s = check_f(p, f, fparam)) return s;
+  const bool want_f = f != RQMC_F_NONE;
+  if (want_f && !h_fsum) return fail(p, RQMC_EINVAL, "f needs h_fsum");
   if (rqmc_status s = upload(p)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(dwork);
@@ -1221,9 +1227,14 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
   const RunRand rr{p->d_shift, p->d_ds, nullptr, 0};
   auto sequence = [&](double* out_host) -> rqmc_status {
     if (rqmc_status s = check_cuda(p, issue_h2d(p, hA, lda, dA, st), "H2D A")) return s;
-    if (rqmc_status s = run_core(p, p->L1, 1, w, p->L1.off_fsum, rr, p->h2d_lv_ev.data(), dA, p->L1.ldr, nullptr,
-                                 0, f, fparam, dsum, st))
+    if (rqmc_status s = run_core(p, p->L1, 1, w, p->L1.off_fsum, rr, p->h2d_lv_ev.data(), dA, p->L1.ldr, dY,
+                                 ldy, f, fparam, want_f ? dsum : nullptr, st))
       return s;
+    if (!want_f) {   // A's staging buffer is read until the run ends: join the copy stream into st
+      cudaError_t ej = cudaEventRecord(p->h2d_ev[1], p->h2d_stream);
+      if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, p->h2d_ev[1], 0);
+      return check_cuda(p, ej, "copy stream join");
+    }
     return check_cuda(p, cudaMemcpyAsync(out_host, dsum, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H fsum");
   };
   // Page-locked A (the bench's pinned buffer): the whole sequence -- the copy-stream fork, the piecewise
@@ -1235,12 +1246,13 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
   static const bool no_graph = RQMC_DEBUG || [] { const char* v = std::getenv("RQMC_NO_GRAPH"); return v && *v && *v != '0'; }();
   if (!pinned || no_graph || p->prof_max > 0) {
     if (rqmc_status s = sequence(h_fsum)) return s;
-    return check_cuda(p, cudaStreamSynchronize(st), "D2H fsum");
+    return check_cuda(p, cudaStreamSynchronize(st), "host run");
   }
   const double fp0 = fparam ? fparam[0] : 0.0, fp1 = fparam ? fparam[1] : 0.0;
   cudaGraphExec_t exec = nullptr;
   for (auto& hg : p->host_graphs)
-    if (hg.hA == hA && hg.dwork == dwork && hg.lda == lda && hg.f == (int)f && hg.fp0 == fp0 && hg.fp1 == fp1)
+    if (hg.hA == hA && hg.dwork == dwork && hg.dY == dY && hg.lda == lda && hg.ldy == ldy && hg.f == (int)f &&
+        hg.fp0 == fp0 && hg.fp1 == fp1)
       exec = hg.exec;
   if (!exec) {
     if (!p->cap_stream) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
@@ -1257,19 +1269,32 @@ rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f,
     if (s != RQMC_OK || e != cudaSuccess || !exec) {   // run directly
       cudaGetLastError();
       if (rqmc_status s2 = sequence(h_fsum)) return s2;
-      return check_cuda(p, cudaStreamSynchronize(st), "D2H fsum");
+      return check_cuda(p, cudaStreamSynchronize(st), "host run");
     }
     if (p->host_graphs.size() >= 8) {
       cudaGraphExecDestroy(p->host_graphs.front().exec);
       p->host_graphs.erase(p->host_graphs.begin());
     }
-    p->host_graphs.push_back({hA, dwork, lda, (int)f, fp0, fp1, exec});
+    p->host_graphs.push_back({hA, dwork, dY, lda, ldy, (int)f, fp0, fp1, exec});
   }
   e = cudaGraphLaunch(exec, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (rqmc_status s = check_cuda(p, e, "host graph")) return s;
-  *h_fsum = *p->h_fsum_pin;
+  if (want_f) *h_fsum = *p->h_fsum_pin;
   return RQMC_OK;
+}
+
+rqmc_status rqmc_qn_host(rqmc_plan_t p, const double* hA, int64_t lda, rqmc_f f, const double* fparam,
+                         double* h_fsum, void* dwork, size_t wbytes, void* stream) {
+  if (!p || !hA || !h_fsum || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+  if (f == RQMC_F_NONE) return fail(p, RQMC_EINVAL, "rqmc_qn_host needs f");
+  return run_host(p, hA, lda, nullptr, 0, f, fparam, h_fsum, dwork, wbytes, stream);
+}
+
+rqmc_status rqmc_xa_host(rqmc_plan_t p, const double* hA, int64_t lda, double* dY, int64_t ldy, rqmc_f f,
+                         const double* fparam, double* h_fsum, void* dwork, size_t wbytes, void* stream) {
+  if (!p || !hA || !dY || !dwork) return fail(p, RQMC_EINVAL, "null pointer");
+  return run_host(p, hA, lda, dY, ldy, f, fparam, h_fsum, dwork, wbytes, stream);
 }
 
 rqmc_status rqmc_workspace_size_batch(rqmc_plan_t p, int R, size_t* bytes) {

@@ -155,3 +155,33 @@ def test_qn_host_pinned_and_pageable(rq, config):
     pin.numpy()[:] = 0.0   # the replayed graph reads the buffer's current contents
     z = float(pl.qn_sum(dev(np.zeros_like(prob.A)), prob.f, prob.fparam).item())
     assert pl.qn_host(pin.numpy(), prob.f, prob.fparam) == z
+
+
+@pytest.mark.parametrize("case", ["C1", "b3"])
+def test_xa_host_pinned_and_pageable(rq, case):
+    """rqmc_xa_host: host A (per-level overlapped H2D, graph-replayed when pinned), Y into a device
+    buffer, the f-sum back to host.  Y and the f-sum equal the device-resident rqmc_xa bit for bit, in
+    pinned, second-buffer, pageable and f = NONE forms, and Y matches the oracle row by row."""
+    if case == "C1":
+        prob = W.make_config("C1")
+    else:
+        prob = W.make_random(241, 3, 8, 150, 70, shifted=True, mapping=W.MAP_INVNORM, f=W.F_MEAN_SQ)
+    pl = rq.Plan.from_problem(prob)
+    Yref, fref = pl.xa(dev(prob.A), prob.f, prob.fparam)
+    Yref = Yref.cpu().numpy()
+    fref = float(fref.item())
+    pin = torch.from_numpy(prob.A.copy()).pin_memory()
+    pin2 = torch.from_numpy(prob.A.copy()).pin_memory()
+    Y = torch.full_like(torch.from_numpy(Yref), float("nan")).cuda()
+    for _ in range(3):
+        assert pl.xa_host(pin.numpy(), Y, prob.f, prob.fparam) == fref
+        assert np.array_equal(Y.cpu().numpy(), Yref)
+    assert pl.xa_host(pin2.numpy(), Y, prob.f, prob.fparam) == fref
+    Y.fill_(float("nan"))
+    assert pl.xa_host(np.array(prob.A, copy=True), Y, prob.f, prob.fparam) == fref   # pageable: direct
+    assert np.array_equal(Y.cpu().numpy(), Yref)
+    Y.fill_(float("nan"))
+    assert pl.xa_host(pin.numpy(), Y) is None                                          # Y only
+    assert np.array_equal(Y.cpu().numpy(), Yref)
+    check_rows(prob, Yref, np.arange(prob.N))
+    check_fsum(prob, fref, np.arange(prob.N))
