@@ -254,7 +254,7 @@ def test_batch_layout_and_workspace(rq):
 def test_run_call_validation(rq):
     """Run-call argument checks of the C ABI return their status before any device work (rqmc.h):
     workspace below rqmc_workspace_size -> EINVAL, lda/ldy < tau -> EDIM, missing / bad f -> EINVAL,
-    batch shift outside [0,1) -> ESHIFT, unshifted plan for a lattice batch -> EINVAL, bad level ->
+    f without a host f-sum slot or no Y (rqmc_xa_host) -> EINVAL, batch shift outside [0,1) -> ESHIFT, unshifted plan for a lattice batch -> EINVAL, bad level ->
     EINVAL.  Fake non-null pointers are never dereferenced on these paths."""
     L = rq.lib()
     p = _plan(rq, shift=[0.1, 0.2, 0.3, 0.4])
@@ -275,6 +275,14 @@ def test_run_call_validation(rq):
     ok = (C.c_double * 8)(*([0.5] * 8))
     assert L.rqmc_qn_batch(q._h, 2, ok, None, None, fake, 3, 0, fp, fs, fake, 1 << 30, st) == 1   # EINVAL
     assert L.rqmc_points(p._h, 99, 0, 1, None, None, st) == 1                           # EINVAL (level)
+    hA = C.cast(C.c_void_p(0x3000), C.POINTER(C.c_double))                           # rqmc_xa_host
+    hs = C.cast(C.c_void_p(0x4000), C.POINTER(C.c_double))
+    assert L.rqmc_xa_host(p._h, hA, 3, fake, 3, 0, fp, hs, fake, need - 1, st) == 1    # EINVAL (workspace)
+    assert L.rqmc_xa_host(p._h, hA, 2, fake, 3, 0, fp, hs, fake, need, st) == 7        # EDIM (lda)
+    assert L.rqmc_xa_host(p._h, hA, 3, fake, 2, 0, fp, hs, fake, need, st) == 7        # EDIM (ldy)
+    assert L.rqmc_xa_host(p._h, hA, 3, None, 3, 0, fp, hs, fake, need, st) == 1        # EINVAL (no Y)
+    assert L.rqmc_xa_host(p._h, hA, 3, fake, 3, 0, fp, None, fake, need, st) == 1      # EINVAL (f, no h_fsum)
+    assert L.rqmc_qn_host(p._h, hA, 3, -1, fp, hs, fake, need, st) == 1                # EINVAL (no f)
 
 
 def test_fine_dispatch_table(rq, monkeypatch):
