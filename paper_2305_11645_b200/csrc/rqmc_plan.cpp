@@ -228,7 +228,10 @@ int fine_smem_bytes(const rqmc_plan_s& p, int c, std::vector<int>* xs_off, std::
   return (int)((2 * as + roots + xs + acc) * sizeof(double));
 }
 
-constexpr int kFineSmemLimit = 200 * 1024;
+#ifndef RQMC_FINE_SMEM_LIMIT_KB   // A/B builds: admit deeper fused subtrees (the kernel's own SMEM still bounds them)
+#define RQMC_FINE_SMEM_LIMIT_KB 200
+#endif
+constexpr int kFineSmemLimit = RQMC_FINE_SMEM_LIMIT_KB * 1024;
 
 // Checkpoint choice: the most fused fine levels subject to depth <= kMaxFine, shared memory, and at
 // least 2 waves of fine CTAs (bundles x replicas >= 2 x 148 SMs) -- replicas of a batched run add

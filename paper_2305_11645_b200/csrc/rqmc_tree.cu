@@ -64,6 +64,9 @@ namespace rqmc {
 #ifndef RQMC_EXP_TB            // exp table bits for g = exp: 6 (64 entries, degree 5) or 11 (2048, degree 3)
 #define RQMC_EXP_TB 6
 #endif
+#ifndef RQMC_TREE43
+#define RQMC_TREE43 0
+#endif
 #ifndef RQMC_TREE_NFR
 #define RQMC_TREE_NFR 4
 #endif
@@ -939,6 +942,9 @@ int tree_select(const FineArgs& a) {
   if (tree_matches<4, 2>(a)) return 42;
   if (tree_matches<3, 2>(a)) return 32;
   if (tree_matches<2, 2>(a)) return 22;
+#if RQMC_TREE43   // A/B builds only: four fused b = 3 levels (C4 with its level-3 GEMM folded in)
+  if (tree_matches<4, 3>(a)) return 43;
+#endif
   if (tree_matches<3, 3>(a)) return 33;
   if (tree_matches<2, 3>(a)) return 23;
   return 0;
@@ -959,6 +965,9 @@ static int64_t tree_split_g(const FineArgs& a, int64_t* nbt) {
 }
 int64_t tree_split(const FineArgs& a, int64_t* nbt) {
   switch (tree_select(a)) {
+#if RQMC_TREE43
+    case 43: return tree_split_g<4, 3>(a, nbt);
+#endif
     case 33: return tree_split_g<3, 3>(a, nbt);
     case 23: return tree_split_g<2, 3>(a, nbt);
     default: *nbt = 0; return 0;   // b = 2 trees never split
@@ -973,6 +982,9 @@ cudaError_t launch_tree(const FineArgs& a, int64_t nb, int nrep, cudaStream_t st
     case 42: return launch_tree_g<4, 2>(a, nb, nrep, st, np);
     case 32: return launch_tree_g<3, 2>(a, nb, nrep, st, np);
     case 22: return launch_tree_g<2, 2>(a, nb, nrep, st, np);
+#if RQMC_TREE43
+    case 43: return launch_tree_g<4, 3>(a, nb, nrep, st, np);
+#endif
     case 33: return launch_tree_g<3, 3>(a, nb, nrep, st, np);
     case 23: return launch_tree_g<2, 3>(a, nb, nrep, st, np);
     default: return cudaErrorNotSupported;
