@@ -28,6 +28,11 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
+__device__ __forceinline__ void pdl_wait() {
+#if RQMC_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 
 // pdl = false: plain stream order (the fused fine-tree kernel: with programmatic launch its CTAs
 // park on the SMs during the checkpoint GEMM's last wave, which measured 0.26 ms slower on C4 with

@@ -602,11 +602,28 @@ __device__ __forceinline__ void tree_clk(int) {}
 // regime); the b = 3 trees (C4: one k_reduce launch is 3 us of 4.5 ms) keep their round-1 code
 template <int NF, int B>
 constexpr bool kFuseReduce = NF <= 4 && B == 2;
+// programmatic launch with the early prologue (above): the same small trees (C2 / C1 regime); the
+// larger trees keep plain stream order (parked CTAs measured slower on C4)
+#ifndef RQMC_TREE_PDL
+#define RQMC_TREE_PDL 1
+#endif
+template <int NF, int B>
+constexpr bool kTreePdl = RQMC_TREE_PDL && kFuseReduce<NF, B>;
 
 template <int NF, int B, int G, bool STY, int NFR, int BUN, int NH>
 __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B, NFR, BUN, NH>::MINB)
     k_fine_tree(const FineArgs a) {
-  pdl_enter();
+  // Early prologue (the small b = 2 trees, launched programmatically after the checkpoint GEMM): the
+  // X^red subtree is issued before the dependency wait -- k_gen wrote it before the GEMM chain, each of
+  // whose kernels waits for its predecessor before it triggers, so k_gen has completed by the time this
+  // grid launches; the root tile (the GEMM's R_c) is read after the wait.  No root (k_gen is the
+  // predecessor itself): wait first.
+  constexpr bool kEarly = kTreePdl<NF, B>;
+  if constexpr (kEarly) {
+    if (a.root == nullptr) pdl_wait();
+  } else {
+    pdl_enter();
+  }
   tree_clk(0);
   using T = Tree<NF, B, NFR, BUN, NH>;
   using Run = TreeRun<NF, B, G, STY, NFR, BUN, NH>;
@@ -657,6 +674,7 @@ __global__ void __launch_bounds__(Tree<NF, B, NFR, BUN, NH>::THREADS, Tree<NF, B
     }
   }
   cp_async_commit();
+  if constexpr (kEarly) pdl_enter();   // the checkpoint GEMM's R_c is visible from here on
 #if RQMC_TREE_CLOCK >= 2
   cp_async_wait<0>();   // phase split (clock builds only): X^red subtree landed
   tree_clk(12);
@@ -906,7 +924,7 @@ static cudaError_t launch_tree_t(const FineArgs& a, int64_t nb, int nrep, cudaSt
   b.nsplit = b.nfull < nbt ? 2 : 1;
   const int64_t grid = b.nfull + (nbt - b.nfull) * b.nsplit;
   return launch_k(k_fine_tree<NF, B, G, STY, NFR, BUN, NH>, dim3((unsigned)grid, (unsigned)nrep), dim3(T::THREADS),
-                  (size_t)smem, st, false, b);
+                  (size_t)smem, st, kTreePdl<NF, B>, b);
 }
 
 // Does the fine level table have the compile-time shape Tree<NF, B> (X^red rows dense, ldx = K)?
