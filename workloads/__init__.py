@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from typing import Optional
 
 import numpy as np
@@ -257,6 +258,8 @@ def make_random(seed: int, b: int, m: int, s: int, tau: int, kind: int = KIND_LA
                 shifted: bool = False, mapping: int = MAP_UNIT, wmode: str = "log",
                 f: int = F_EXP_MEAN, int_a: bool = False) -> Problem:
     """Small random problems for property sweeps: random nondecreasing w with w_1 = 0."""
+    # RQMC_TEST_SEED_OFFSET (tools/fuzz_parity.sh): the same sweeps on other seeds; both sides get the same inputs
+    seed = seed + int(os.environ.get("RQMC_TEST_SEED_OFFSET", "0") or 0)
     rng = stream(seed, 99, 4 * s + 8)
     if wmode == "log":
         w = w_log(b, m, s)
