@@ -4,7 +4,7 @@ f-sums (Y stored and not) against the CPU oracle at the tests' tolerances (1e-12
 |A_c|_1 per entry; relative 1e-12 of sum |f_k|).  The sizes reach the fused fine kernels (b = 2 up to
 m = 16, b = 3 up to m = 10) with ragged s and tau.  Test tooling: it calls oracle/ like tests/ do.
 
-usage: python tools/fuzz_shapes.py --seed 1 --cases 150 [--budget-s 600]
+usage: python tools/fuzz_shapes.py --seed 1 --cases 150 [--budget-s 600] [--fft]
 """
 import argparse
 import os
@@ -123,7 +123,12 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cases", type=int, default=100)
     ap.add_argument("--budget-s", type=float, default=900.0)
+    ap.add_argument("--fft", action="store_true",
+                    help="RQMC_FFT=1: every eligible coarse level (unshifted b = 2 lattices) on the FFT product, "
+                         "and only such problems are drawn")
     a = ap.parse_args()
+    if a.fft:
+        os.environ["RQMC_FFT"] = "1"
     assert torch.cuda.is_available(), "needs cuda:0"
     rng = np.random.default_rng(a.seed)
     t0 = time.time()
@@ -133,6 +138,12 @@ def main():
         if time.time() - t0 > a.budget_s:
             break
         c = draw_case(rng)
+        if a.fft:
+            c.update(b=2, kind=W.KIND_LATTICE, shifted=False, m=max(c["m"] if c["b"] == 2 else 3 + c["m"], 3))
+            if c["ck"] and rng.random() < 0.5:
+                c["ck"] = "0"      # every level coarse
+            while 2 ** c["m"] * c["s"] * c["tau"] > 1.5e9:
+                c["tau"] = max(1, c["tau"] // 2)
         res = run_case(100000 * a.seed + i, c)
         tag = res.split()[0]
         if tag == "ok":
